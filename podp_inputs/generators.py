@@ -1,0 +1,246 @@
+"""Seeded generators (see package docstring).  All complex data complex128, row-major (C order).
+
+Draw order is part of the contract; changing it changes every seeded input.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+MU0 = 4.0 * math.pi * 1e-7  # PAPER.md P:159, mu_0 = 4 pi 1e-7 exactly (reading U15)
+# BASELINE.json configs[0]: nu = mu0 * sigma * alpha^2 = 4 pi 1e-7 * 5.96e7 * (1e-2)^2 (omega-free; paper's nu-tilde)
+NU_DEFAULT = MU0 * 5.96e7 * (1e-2) ** 2
+ALPHA_DEFAULT = 1e-2
+
+
+@dataclasses.dataclass
+class Operators:
+    """Inputs of podp_create for one object (shared reduced basis, BASELINE form).
+
+    K, M, K_R: r x r Hermitian; b0, b1: r x 3 (column i = direction i); N0, S: 3 x 3 real symmetric;
+    H: 3 x r (row i = h_i, unconjugated); G: (6+2r) x (6+2r) Hermitian PSD Gram, slot order
+    [b0_1, b1_1, b0_2, b1_2, b0_3, b1_3 | K U (r) | M U (r)].
+    """
+    K: np.ndarray
+    M: np.ndarray
+    b0: np.ndarray
+    b1: np.ndarray
+    N0: np.ndarray
+    S: np.ndarray
+    H: np.ndarray
+    G: np.ndarray
+    nu: float
+    alpha: float
+    alpha_lb: float
+    K_R: np.ndarray | None = None
+
+    @property
+    def r(self) -> int:
+        return int(self.K.shape[0])
+
+    def copy(self) -> "Operators":
+        return dataclasses.replace(self, **{f.name: (np.array(getattr(self, f.name)) if isinstance(getattr(self, f.name), np.ndarray) else getattr(self, f.name))
+                                            for f in dataclasses.fields(self)})
+
+
+@dataclasses.dataclass
+class Config0Extras:
+    """Full-order objects of the tiny config 0 (oracle-side full-order checks only)."""
+    K_full: np.ndarray
+    M_full: np.ndarray
+    C_full: np.ndarray       # nu * M_full
+    U: np.ndarray            # N x r orthonormal
+    v: np.ndarray            # N x 3 real (theta0-tilde + e_i x xi coefficients, conductor dofs)
+    B0f: np.ndarray          # N x 3 full-order source, omega^0 part
+    B1f: np.ndarray          # N x 3 full-order source, omega^1 part
+    W: np.ndarray            # N x (6+2r) residual factor, G = W^H W
+
+
+def cn(rng: np.random.Generator, shape, var: float) -> np.ndarray:
+    """CN(0, var): sqrt(var/2) * (N(0,1) + i N(0,1)); the whole real array is drawn first (reading U16)."""
+    re = rng.standard_normal(shape)
+    im = rng.standard_normal(shape)
+    return math.sqrt(var / 2.0) * (re + 1j * im)
+
+
+def _herm(X: np.ndarray) -> np.ndarray:
+    return 0.5 * (X + X.conj().T)
+
+
+def omega_grid(F: int, lo: float = 1e1, hi: float = 1e8) -> np.ndarray:
+    """F log-spaced output frequencies on [lo, hi] rad/s (BASELINE configs)."""
+    return np.logspace(math.log10(lo), math.log10(hi), F)
+
+
+def snapshot_grid(N: int = 13, lo: float = 1e1, hi: float = 1e8) -> np.ndarray:
+    """Initial log-spaced snapshot set, N = 13 on [1e1, 1e8] (Algorithm 1 line 3; reading U14)."""
+    return np.logspace(math.log10(lo), math.log10(hi), N)
+
+
+def embed_gram(G1: np.ndarray, r: int) -> np.ndarray:
+    """Embed the literal (2+2r) Gram into the stacked (6+2r) slot order (reading U9): G[u,v] = G1[pi(u), pi(v)]."""
+    pi = np.array([0, 1, 0, 1, 0, 1] + list(range(2, 2 + 2 * r)))
+    return G1[np.ix_(pi, pi)].copy()
+
+
+def make_operators(r: int, seed: int = 0, nu: float = NU_DEFAULT, alpha: float = ALPHA_DEFAULT,
+                   alpha_lb: float = 1.0) -> Operators:
+    """Config 1/2/4 generator (BASELINE.json configs[1]; SURVEY.md 8(d) draw order (1)..(6))."""
+    if r < 2 or r % 2:
+        raise ValueError("r must be even and >= 2 (M has rank r/2)")
+    rng = np.random.default_rng(seed)
+    B = cn(rng, (r, r), 1.0 / r)
+    K = _herm(B @ B.conj().T + r * np.eye(r))
+    C = cn(rng, (r, r // 2), 1.0 / r)
+    M = _herm(C @ C.conj().T)
+    b0 = cn(rng, (r, 3), 1.0)
+    b1 = cn(rng, (r, 3), 1.0)
+    Sr = rng.standard_normal((3, 3))
+    S = np.triu(Sr) + np.triu(Sr, 1).T
+    H = cn(rng, (3, r), 1.0)
+    W = cn(rng, (2 * (2 + 2 * r), 2 + 2 * r), 1.0)
+    G1 = W.conj().T @ W
+    G = embed_gram(G1, r)
+    return Operators(K=K, M=M, b0=b0, b1=b1, N0=np.eye(3), S=S, H=H, G=G, nu=float(nu), alpha=float(alpha),
+                     alpha_lb=float(alpha_lb))
+
+
+def batch_sigma(n_obj: int = 256) -> np.ndarray:
+    """Config 3 conductivities: log-uniform in [1e6, 6e7] S/m from a separate stream (SURVEY 8(d) proposal)."""
+    return 10.0 ** np.random.default_rng(0).uniform(6.0, math.log10(6e7), n_obj)
+
+
+def make_config0(seed: int = 0, N: int = 2000, r: int = 8, nu: float = NU_DEFAULT, alpha: float = ALPHA_DEFAULT,
+                 alpha_lb: float = 0.1):
+    """Tiny config 0: synthetic full-order system N=2000 projected onto an orthonormal U (BASELINE configs[0]).
+
+    Returns (Operators, Config0Extras). Draw order (1)..(8) of SURVEY.md 8(d).
+    """
+    rng = np.random.default_rng(seed)
+    nnz_per_row = 8
+    cols = rng.integers(0, N, nnz_per_row * N)
+    vals = cn(rng, (nnz_per_row * N,), 1.0)
+    A = np.zeros((N, N), dtype=np.complex128)
+    rows = np.repeat(np.arange(N), nnz_per_row)
+    np.add.at(A, (rows, cols), vals)
+    K_full = _herm(A.conj().T @ A + 0.1 * np.eye(N))
+    Nc = N // 2
+    Cc = cn(rng, (1000, Nc), 1.0)
+    M_full = np.zeros((N, N), dtype=np.complex128)
+    M_full[:Nc, :Nc] = Cc.conj().T @ Cc
+    M_full = _herm(M_full)
+    U, _ = np.linalg.qr(cn(rng, (N, r), 1.0))
+    K = _herm(U.conj().T @ K_full @ U)
+    M = _herm(U.conj().T @ M_full @ U)
+    b0 = cn(rng, (r, 3), 1.0)
+    b1 = cn(rng, (r, 3), 1.0)
+    v = np.zeros((N, 3))
+    v[:Nc] = rng.standard_normal((Nc, 3))
+    C_full = nu * M_full
+    S = np.real(v.T @ C_full @ v)
+    S = 0.5 * (S + S.T)
+    H = v.T @ C_full @ U
+    z0 = cn(rng, (N, 3), 1.0)
+    z1 = cn(rng, (N, 3), 1.0)
+    Pperp = lambda z: z - U @ (U.conj().T @ z)  # noqa: E731
+    B0f = U @ b0 + Pperp(z0)
+    B1f = U @ b1 + Pperp(z1)
+    W = np.zeros((N, 6 + 2 * r), dtype=np.complex128)
+    for i in range(3):
+        W[:, 2 * i] = B0f[:, i]
+        W[:, 2 * i + 1] = B1f[:, i]
+    W[:, 6:6 + r] = K_full @ U
+    W[:, 6 + r:] = M_full @ U
+    G = _herm(W.conj().T @ W)
+    ops = Operators(K=K, M=M, b0=b0, b1=b1, N0=np.eye(3), S=S, H=H, G=G, nu=float(nu), alpha=float(alpha),
+                    alpha_lb=float(alpha_lb))
+    return ops, Config0Extras(K_full=K_full, M_full=M_full, C_full=C_full, U=U, v=v, B0f=B0f, B1f=B1f, W=W)
+
+
+def make_galerkin_variant(ops: Operators, ex: Config0Extras, seed: int = 1):
+    """Pin C3 input: b0 = U^H K_full U y, b1 = i nu U^H M_full U y with full-order sources in span(K U y), so the
+    exact full-order solution is U y for every omega.  Returns (ops', ex', y)."""
+    rng = np.random.default_rng(seed)
+    r = ops.r
+    y = cn(rng, (r, 3), 1.0)
+    B0f = ex.K_full @ (ex.U @ y)
+    B1f = 1j * ops.nu * (ex.M_full @ (ex.U @ y))
+    b0 = ex.U.conj().T @ B0f
+    b1 = ex.U.conj().T @ B1f
+    W = ex.W.copy()
+    for i in range(3):
+        W[:, 2 * i] = B0f[:, i]
+        W[:, 2 * i + 1] = B1f[:, i]
+    G = _herm(W.conj().T @ W)
+    ops2 = dataclasses.replace(ops, b0=b0, b1=b1, G=G)
+    ex2 = dataclasses.replace(ex, B0f=B0f, B1f=B1f, W=W)
+    return ops2, ex2, y
+
+
+def make_identity_basis_variant(seed: int = 0, r: int = 8, nu: float = NU_DEFAULT, alpha: float = ALPHA_DEFAULT):
+    """Pin C5 input: N = r, U = I (full order == reduced order)."""
+    return make_config0(seed=seed, N=2 * r, r=r, nu=nu, alpha=alpha)  # N=2r keeps a conductor half; U from QR
+
+
+def pad_operators(ops: Operators, r_pad: int) -> Operators:
+    """Exact padding: K_pad = diag(K, I); M, K_R, b, H, G zero-padded (G in both r-blocks)."""
+    r = ops.r
+    if r_pad < r:
+        raise ValueError("r_pad < r")
+    def pad_sq(X, eye):
+        Y = np.zeros((r_pad, r_pad), dtype=np.complex128)
+        Y[:r, :r] = X
+        if eye:
+            Y[r:, r:] = np.eye(r_pad - r)
+        return Y
+    def pad_rows(X):
+        Y = np.zeros((r_pad, X.shape[1]), dtype=np.complex128)
+        Y[:r] = X
+        return Y
+    H = np.zeros((3, r_pad), dtype=np.complex128)
+    H[:, :r] = ops.H
+    n, n2 = 6 + 2 * r, 6 + 2 * r_pad
+    idx = np.concatenate([np.arange(6), 6 + np.arange(r), 6 + r_pad + np.arange(r)])
+    G = np.zeros((n2, n2), dtype=np.complex128)
+    G[np.ix_(idx, idx)] = ops.G[:n, :n]
+    return dataclasses.replace(ops, K=pad_sq(ops.K, True), M=pad_sq(ops.M, False),
+                               K_R=None if ops.K_R is None else pad_sq(ops.K_R, False),
+                               b0=pad_rows(ops.b0), b1=pad_rows(ops.b1), H=H, G=G)
+
+
+_CONFIGS = {
+    0: dict(name="c0_tiny_r8_F200", r=8, F=200, n_obj=1),
+    1: dict(name="c1_r24_F1e4", r=24, F=10_000, n_obj=1),
+    2: dict(name="c2_r48_F1e5", r=48, F=100_000, n_obj=1),
+    3: dict(name="c3_dict256_r32_F2000", r=32, F=2_000, n_obj=256),
+    4: dict(name="c4_r96_F1e6_select", r=96, F=1_000_000, n_obj=1, n_snap=13, n_star=2),
+}
+
+
+def config_spec(k: int) -> dict:
+    return dict(_CONFIGS[k])
+
+
+def make_config(k: int, F: int | None = None, n_obj: int | None = None):
+    """Return dict(spec, ops=[Operators per object], omega, extras) for BASELINE config k (F/n_obj overridable)."""
+    spec = config_spec(k)
+    if F is not None:
+        spec["F"] = int(F)
+    if n_obj is not None:
+        spec["n_obj"] = int(n_obj)
+    omega = omega_grid(spec["F"])
+    extras = None
+    if k == 0:
+        ops, extras = make_config0()
+        ops_list = [ops]
+    elif k == 3:
+        sig = batch_sigma(256)
+        ops_list = [make_operators(spec["r"], seed=j, nu=MU0 * sig[j] * ALPHA_DEFAULT ** 2) for j in range(spec["n_obj"])]
+    else:
+        ops_list = [make_operators(spec["r"], seed=0)]
+    out = dict(spec=spec, ops=ops_list, omega=omega, extras=extras)
+    if k == 4:
+        out["snap"] = snapshot_grid(spec["n_snap"])
+    return out
