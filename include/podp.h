@@ -1,0 +1,143 @@
+/* podp.h -- C ABI of libpodp: the on-line stage of projected POD (PODP) for magnetic polarizability tensor
+ * (MPT) spectral signatures, arXiv 2307.05590 (Elgy & Ledger), on one NVIDIA B200 (sm_100a), FP64.
+ *
+ * Citations: "P:<line>" = PAPER.md (the paper's LaTeX), with the section / equation label it falls in.
+ *
+ * What one evaluation computes, for every output frequency omega (Algorithm 1 lines 22-26):
+ *   a2  A(omega) = K + i*omega*nu*M,  B(omega) = b0 + omega*b1            (eqn:ReducedA; BASELINE sign)
+ *   a3  P(omega) = A(omega)^{-1} B(omega)  (r x 3; column i = p_i)        (eqn:ReducedA)
+ *   a4  R_ij = -(alpha^3/4) Re(p_i^H K_R p_j),  Rt = N0 + R               (eqn:podprealmpt P:600-604; eqn:NRI P:440)
+ *       I_ij = (omega alpha^3/4) (S_ij + nu Re(p_i^H M p_j) + Re(h_i p_j) + Re(h_j p_i))
+ *                                                                          (eqn:podpimagmpt P:606-620, shared basis)
+ *   a5  X_ij = w_i^H G w_j with w_i = [e_{2i} + omega e_{2i+1} | -p_i | -i omega nu p_i]
+ *       n_i = max(0, Re X_ii), m_ij = max(0, n_i + n_j - 2 Re X_ij),
+ *       Delta_ij = alpha^3/(8 alpha_LB) (n_i + n_j + m_ij)                 (lemma:certificate)
+ *   a6  outputs: Rt (or R), I, Delta as F x 6 row-major doubles, entry order (11,22,33,12,13,23)
+ *   a7  podp_select: one greedy step of Algorithm 1
+ *
+ * Conventions (all functions):
+ *   - complex = interleaved (re, im) double pairs, i.e. C99 double _Complex / numpy complex128 /
+ *     torch.complex128.  Declared here as `const double *` pointing at 2*n doubles.
+ *   - ALL matrices are ROW-MAJOR (C order), matching NumPy/PyTorch.  A Hermitian matrix passed transposed
+ *     arrives as its conjugate and silently conjugates the results (SURVEY "layout trap"); there is no check.
+ *   - No function aborts, throws or exits across the ABI.  Every non-OK status sets a thread-local message
+ *     readable with podp_last_error().
+ *   - "device" pointers are CUDA device pointers on the context's device; "host" pointers are CPU memory
+ *     (pinned memory makes the host-buffer entry points faster but is not required).
+ *   - cuda_stream is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef PODP_H
+#define PODP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PODP_R_MAX 128          /* largest supported number of POD modes r (configs need <= 96) */
+#define PODP_SNAP_MAX 1025      /* largest snapshot set accepted by podp_select (<= 1024 intervals) */
+
+typedef struct podp_ctx podp_ctx; /* opaque; owns packed device copies of the operators; read-only after create */
+
+typedef enum {
+  PODP_OK = 0,
+  PODP_ERR_ARG = 1,           /* invalid argument (null pointer, r out of range, F < 0, nu/alpha/alpha_lb <= 0, ...) */
+  PODP_ERR_CUDA = 2,          /* a CUDA runtime call or kernel launch failed */
+  PODP_ERR_OOM = 3,           /* device or pinned-host allocation failed */
+  PODP_ERR_UNSUPPORTED = 4,   /* e.g. device is not sm_100 */
+  PODP_ERR_NONFINITE = 5,     /* a non-finite value in an operator input */
+  PODP_ERR_NOT_HERMITIAN = 6, /* K, M, K_R or G has a Hermitian defect above 1e-12 * max|X| */
+  PODP_ERR_NO_CANDIDATES = 7  /* podp_select: fewer non-empty intervals than requested */
+} podp_status;
+
+enum {
+  PODP_FLAG_DEFAULT = 0,        /* first output = Rt = N0 + R                                              */
+  PODP_FLAG_OUT_R = 1u << 0,    /* first output = omega-dependent R only (used by parity runs, reading U11)  */
+  PODP_FLAG_OUT_P = 1u << 1,    /* debug: also write P (n_obj x F x 3 x r complex, row-major) to P_d       */
+  PODP_FLAG_NO_PIVOT = 1u << 2  /* LU without pivoting (exists since Re x^H A x = x^H K x > 0 for K > 0;
+                                   SURVEY Appendix A.4).  Default is partial pivoting.                       */
+};
+
+/* Operators of ONE object (host pointers; copied, validated and packed by podp_create; caller keeps ownership).
+ * r = number of POD modes (paper's M).  Shared reduced basis (BASELINE reading U3). */
+typedef struct {
+  int32_t r;            /* 1 <= r <= PODP_R_MAX                                                                 */
+  double nu;            /* mu0*sigma*alpha^2 > 0, omega-free (paper's nu-tilde)                           */
+  double alpha;         /* object size alpha > 0; enters as alpha^3/4 and alpha^3/(8 alpha_LB)                   */
+  double alpha_lb;      /* stability lower bound alpha_LB > 0 (lemma:certificate)                        */
+  const double *K;      /* r x r complex Hermitian: reduced system stiffness (incl. eps*M_reg)            */
+  const double *M;      /* r x r complex Hermitian PSD: nu-free reduced conductor mass (C^M / nu)         */
+  const double *K_R;    /* r x r complex Hermitian, or NULL (= K): stiffness used in R (reading U4)             */
+  const double *b0;     /* r x 3 complex (row-major; column i = direction i): omega^0 part of r_i^M (reading U2) */
+  const double *b1;     /* r x 3 complex: omega^1 part of r_i^M                                                  */
+  const double *N0;     /* 3 x 3 real symmetric: N^0 (omega-independent)                           */
+  const double *S;      /* 3 x 3 real symmetric: o_i^T C1 o_j + c_ij + s_i^T o_j + s_j^T o_i  */
+  const double *H;      /* 3 x r complex: row i = h_i = o_i^T C2 U + t_i^T U (unconjugated)           */
+  const double *G;      /* (6+2r) x (6+2r) complex Hermitian PSD Gram of the residual factor, slot order
+                           [b0_1, b1_1, b0_2, b1_2, b0_3, b1_3 | K U (r) | M U (r)]  (reading U9)     */
+} podp_operators;
+
+/* Validate + pack one object's operators onto `device`; the upload is enqueued on cuda_stream and complete
+ * when podp_create returns.  Returns PODP_ERR_ARG / _NONFINITE / _NOT_HERMITIAN / _OOM / _CUDA / _UNSUPPORTED. */
+podp_status podp_create(const podp_operators *ops, int device, void *cuda_stream, podp_ctx **out);
+
+/* Same for n_obj >= 1 independent objects (dictionary batch, BASELINE config 3); all must share r. */
+podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int device, void *cuda_stream,
+                              podp_ctx **out);
+
+/* Device-buffer evaluation (the hot path).  Asynchronous on cuda_stream; no host synchronisation.
+ *   omega_d : device, F doubles (the same output grid for every object)
+ *   T1_d    : device, n_obj x F x 6 doubles: Rt = N0 + R (default) or R (PODP_FLAG_OUT_R)
+ *   I_d     : device, n_obj x F x 6 doubles
+ *   Delta_d : device, n_obj x F x 6 doubles
+ *   info_d  : device, n_obj x F int32, nullable: 0 = ok; k+1 = exactly-zero pivot at step k (LAPACK getrf
+ *             convention); -1 = non-finite omega.  Failed rows of T1/I/Delta are NaN; other rows unaffected.
+ *   P_d     : device, n_obj x F x 3 x r complex (only read if PODP_FLAG_OUT_P, else may be NULL)
+ * F == 0 is a no-op.  Outputs are caller-owned; the context is not modified (concurrent evals on different
+ * streams with distinct outputs are safe). */
+podp_status podp_eval(const podp_ctx *ctx, const double *omega_d, int64_t F, double *T1_d, double *I_d,
+                      double *Delta_d, int32_t *info_d, double *P_d, int flags, void *cuda_stream);
+
+/* Host-buffer evaluation (the end-to-end entry point): copies omega host->device, runs podp_eval, copies the
+ * outputs device->host and synchronises cuda_stream before returning.  Same shapes as podp_eval, all host. */
+podp_status podp_eval_host(const podp_ctx *ctx, const double *omega_h, int64_t F, double *T1_h, double *I_h,
+                           double *Delta_h, int32_t *info_h, int flags, void *cuda_stream);
+
+/* One greedy step of Algorithm 1 (P:677-682 lines 10-15) on object `obj` of the context's layout:
+ *   intervals [snap_n, snap_{n+1}), n = 0..n_snap-2, the last one closed (reading U12); grid points equal to a
+ *   snapshot or outside [snap_0, snap_{n_snap-1}] are not candidates; NaN Delta entries are ignored.
+ *   Lambda_n = max over in-interval omega and the 6 entries of Delta; argmax = lowest grid index among ties.
+ *   theta <= 0: choose the n_star intervals with the largest Lambda_n (ties -> lower n);
+ *   0 < theta <= 1: choose intervals with Lambda_n >= theta * Lambda (at most n_star, largest first).
+ *   omega_d, Delta_d: device (F and F x 6 doubles, e.g. podp_eval outputs for that object);
+ *   snap_omega: host, strictly ascending, 2 <= n_snap <= PODP_SNAP_MAX;
+ *   outputs (host): *n_new chosen (<= n_star), omega_new[n_star] ascending, idx_new[n_star] grid indices,
+ *   *Lambda global max, Lambda_n[n_snap-1] per-interval maxima (nullable; -1 for empty intervals).
+ *   Synchronises cuda_stream.  PODP_ERR_NO_CANDIDATES if theta <= 0 and fewer than n_star intervals are non-empty
+ *   (or no interval is non-empty). */
+podp_status podp_select(const podp_ctx *ctx, const double *omega_d, const double *Delta_d, int64_t F,
+                        const double *snap_omega, int32_t n_snap, int32_t n_star, double theta, int32_t *n_new,
+                        double *omega_new, int64_t *idx_new, double *Lambda, double *Lambda_n,
+                        void *cuda_stream);
+
+/* Number of objects / modes of a context (0 if ctx is NULL). */
+int32_t podp_n_obj(const podp_ctx *ctx);
+int32_t podp_r(const podp_ctx *ctx);
+
+/* Number of kernel launches the last podp_eval on this thread enqueued (bench bookkeeping). */
+int32_t podp_last_launch_count(void);
+
+/* Release a context (NULL-safe; synchronises the device work that used it is the caller's job). */
+podp_status podp_destroy(podp_ctx *ctx);
+
+/* Thread-local message of the last non-OK status ("" if none). */
+const char *podp_last_error(void);
+
+/* Library version string. */
+const char *podp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PODP_H */

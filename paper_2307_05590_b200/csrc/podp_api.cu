@@ -1,0 +1,381 @@
+// libpodp C ABI (include/podp.h): validation, packing (row a1 of SURVEY 8(a)), launch orchestration.
+// Host-side only; kernels live in k_solve.cu (a2-a3), k_mpt.cu (a4-a6) and k_select.cu (a7).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "podp_internal.h"
+
+struct podp_ctx {
+  int device;
+  int r;
+  int n_obj;
+  podp::Layout L;
+  double *d_ops;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_last_launches = 0;
+
+podp_status fail(podp_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+podp_status cuda_fail(cudaError_t e, const char *what) {
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation) return fail(PODP_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+  return fail(PODP_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Saves/restores the caller's current device.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool all_finite(const double *x, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+// Hermitian defect max|X - X^H| <= 1e-12 max|X| (SURVEY 8(b) "Errors")
+bool is_hermitian(const double *X, int n) {
+  double mx = 0.0, defect = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double re = X[2 * (i * n + j)], im = X[2 * (i * n + j) + 1];
+      mx = std::fmax(mx, std::hypot(re, im));
+      const double tre = X[2 * (j * n + i)], tim = -X[2 * (j * n + i) + 1];
+      defect = std::fmax(defect, std::hypot(re - tre, im - tim));
+    }
+  return defect <= 1e-12 * mx;
+}
+
+bool is_symmetric3(const double *X) {
+  double mx = 0.0, defect = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      mx = std::fmax(mx, std::fabs(X[i * 3 + j]));
+      defect = std::fmax(defect, std::fabs(X[i * 3 + j] - X[j * 3 + i]));
+    }
+  return defect <= 1e-12 * mx;
+}
+
+podp_status validate(const podp_operators &o, int idx) {
+  if (o.r < 1 || o.r > PODP_R_MAX) return fail(PODP_ERR_ARG, "object %d: r=%d out of range [1,%d]", idx, o.r, PODP_R_MAX);
+  if (!o.K || !o.M || !o.b0 || !o.b1 || !o.N0 || !o.S || !o.H || !o.G)
+    return fail(PODP_ERR_ARG, "object %d: null operator pointer", idx);
+  if (!(o.nu > 0.0) || !std::isfinite(o.nu)) return fail(PODP_ERR_ARG, "object %d: nu must be finite and > 0", idx);
+  if (!(o.alpha > 0.0) || !std::isfinite(o.alpha)) return fail(PODP_ERR_ARG, "object %d: alpha must be finite and > 0", idx);
+  if (!(o.alpha_lb > 0.0) || !std::isfinite(o.alpha_lb))
+    return fail(PODP_ERR_ARG, "object %d: alpha_lb must be finite and > 0", idx);
+  const int r = o.r, ng = 6 + 2 * r;
+  const size_t rr = (size_t)2 * r * r;
+  if (!all_finite(o.K, rr) || !all_finite(o.M, rr) || (o.K_R && !all_finite(o.K_R, rr)) ||
+      !all_finite(o.b0, 6 * (size_t)r) || !all_finite(o.b1, 6 * (size_t)r) || !all_finite(o.N0, 9) ||
+      !all_finite(o.S, 9) || !all_finite(o.H, 6 * (size_t)r) || !all_finite(o.G, (size_t)2 * ng * ng))
+    return fail(PODP_ERR_NONFINITE, "object %d: non-finite operator entry", idx);
+  if (!is_hermitian(o.K, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: K is not Hermitian", idx);
+  if (!is_hermitian(o.M, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: M is not Hermitian", idx);
+  if (o.K_R && !is_hermitian(o.K_R, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: K_R is not Hermitian", idx);
+  if (!is_hermitian(o.G, ng)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: G is not Hermitian", idx);
+  if (!is_symmetric3(o.S) || !is_symmetric3(o.N0)) return fail(PODP_ERR_ARG, "object %d: S / N0 not symmetric", idx);
+  return PODP_OK;
+}
+
+// Pack one object into dst (L.stride doubles, zero-initialised by the caller).
+void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
+  const int r = o.r, R = L.R, ng = 6 + 2 * r;
+  auto C = [](const double *X, int ld, int i, int j, int comp) { return X[2 * ((size_t)i * ld + j) + comp]; };
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) {
+      const bool in = i < r && j < r;
+      for (int c = 0; c < 2; ++c) {
+        const size_t e = 2 * ((size_t)i * R + j) + c;
+        dst[L.K + e] = in ? C(o.K, r, i, j, c) : (i == j && c == 0 ? 1.0 : 0.0);  // K_pad = diag(K, I)
+        dst[L.M + e] = in ? C(o.M, r, i, j, c) : 0.0;
+        dst[L.KR + e] = in ? C(o.K_R ? o.K_R : o.K, r, i, j, c) : 0.0;
+        dst[L.Gkk + e] = in ? C(o.G, ng, 6 + i, 6 + j, c) : 0.0;
+        dst[L.Gmm + e] = in ? C(o.G, ng, 6 + r + i, 6 + r + j, c) : 0.0;
+      }
+      // J = i (G_KM - G_MK): re = -(Im G_KM - Im G_MK), im = Re G_KM - Re G_MK
+      if (in) {
+        const double kmr = C(o.G, ng, 6 + i, 6 + r + j, 0), kmi = C(o.G, ng, 6 + i, 6 + r + j, 1);
+        const double mkr = C(o.G, ng, 6 + r + i, 6 + j, 0), mki = C(o.G, ng, 6 + r + i, 6 + j, 1);
+        dst[L.J + 2 * ((size_t)i * R + j)] = -(kmi - mki);
+        dst[L.J + 2 * ((size_t)i * R + j) + 1] = kmr - mkr;
+      }
+    }
+  for (int c3 = 0; c3 < 3; ++c3)
+    for (int i = 0; i < r; ++i)
+      for (int c = 0; c < 2; ++c) {
+        dst[L.b0 + 2 * ((size_t)c3 * R + i) + c] = o.b0[2 * ((size_t)i * 3 + c3) + c];
+        dst[L.b1 + 2 * ((size_t)c3 * R + i) + c] = o.b1[2 * ((size_t)i * 3 + c3) + c];
+        dst[L.H + 2 * ((size_t)c3 * R + i) + c] = o.H[2 * ((size_t)c3 * r + i) + c];
+      }
+  for (int a = 0; a < 6; ++a) {
+    for (int i = 0; i < r; ++i)
+      for (int c = 0; c < 2; ++c) {
+        dst[L.GbK + 2 * ((size_t)a * R + i) + c] = C(o.G, ng, a, 6 + i, c);
+        dst[L.GbM + 2 * ((size_t)a * R + i) + c] = C(o.G, ng, a, 6 + r + i, c);
+      }
+    for (int b = 0; b < 6; ++b)
+      for (int c = 0; c < 2; ++c) dst[L.Gbb + 2 * (a * 6 + b) + c] = C(o.G, ng, a, b, c);
+  }
+  double *sc = dst + L.scal;
+  sc[podp::SC_NU] = o.nu;
+  sc[podp::SC_ALPHA] = o.alpha;
+  sc[podp::SC_ALPHA_LB] = o.alpha_lb;
+  for (int e = 0; e < 9; ++e) {
+    sc[podp::SC_S + e] = o.S[e];
+    sc[podp::SC_N0 + e] = o.N0[e];
+  }
+}
+
+int choose_R(int r) { return r; }
+
+}  // namespace
+
+namespace podp {
+Layout make_layout(int R) {
+  Layout L;
+  L.R = R;
+  int64_t off = 0;
+  auto take = [&](int64_t n) {
+    int64_t o = off;
+    off += (n + 31) / 32 * 32;  // 256-byte aligned blocks
+    return o;
+  };
+  const int64_t sq = 2LL * R * R, vec3 = 6LL * R, vec6 = 12LL * R;
+  L.K = take(sq);
+  L.M = take(sq);
+  L.KR = take(sq);
+  L.Gkk = take(sq);
+  L.J = take(sq);
+  L.Gmm = take(sq);
+  L.b0 = take(vec3);
+  L.b1 = take(vec3);
+  L.H = take(vec3);
+  L.GbK = take(vec6);
+  L.GbM = take(vec6);
+  L.Gbb = take(72);
+  L.scal = take(SCAL_N);
+  L.stride = off;
+  return L;
+}
+}  // namespace podp
+
+extern "C" {
+
+const char *podp_last_error(void) { return g_err.c_str(); }
+const char *podp_version(void) { return "podp-b200 0.1 (sm_100a, fp64)"; }
+int32_t podp_last_launch_count(void) { return g_last_launches; }
+int32_t podp_n_obj(const podp_ctx *c) { return c ? c->n_obj : 0; }
+int32_t podp_r(const podp_ctx *c) { return c ? c->r : 0; }
+
+podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int device, void *cuda_stream,
+                              podp_ctx **out) {
+  g_err.clear();
+  if (!out) return fail(PODP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_obj < 1 || !ops) return fail(PODP_ERR_ARG, "n_obj must be >= 1 and ops non-NULL");
+  for (int k = 0; k < n_obj; ++k) {
+    podp_status st = validate(ops[k], k);
+    if (st != PODP_OK) return st;
+    if (ops[k].r != ops[0].r) return fail(PODP_ERR_ARG, "object %d: r=%d differs from object 0 (r=%d)", k, ops[k].r, ops[0].r);
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) return fail(PODP_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10) return fail(PODP_ERR_UNSUPPORTED, "device %d is sm_%d%d; libpodp is built for sm_100a", device, prop.major, prop.minor);
+  DeviceGuard guard(device);
+  if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+  const int r = ops[0].r;
+  podp::Layout L = podp::make_layout(choose_R(r));
+  std::vector<double> host((size_t)L.stride * n_obj, 0.0);
+  for (int k = 0; k < n_obj; ++k) pack(ops[k], L, host.data() + (size_t)L.stride * k);
+  double *d = nullptr;
+  e = cudaMalloc(&d, host.size() * sizeof(double));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(operators)");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  e = cudaMemcpyAsync(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(e, "upload operators");
+  }
+  podp_ctx *c = new podp_ctx;
+  c->device = device;
+  c->r = r;
+  c->n_obj = n_obj;
+  c->L = L;
+  c->d_ops = d;
+  *out = c;
+  return PODP_OK;
+}
+
+podp_status podp_create(const podp_operators *ops, int device, void *cuda_stream, podp_ctx **out) {
+  return podp_create_batch(1, ops, device, cuda_stream, out);
+}
+
+podp_status podp_destroy(podp_ctx *c) {
+  if (!c) return PODP_OK;
+  DeviceGuard guard(c->device);
+  cudaFree(c->d_ops);
+  delete c;
+  return PODP_OK;
+}
+
+podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, double *T1_d, double *I_d,
+                      double *Delta_d, int32_t *info_d, double *P_d, int flags, void *cuda_stream) {
+  g_err.clear();
+  g_last_launches = 0;
+  if (!c) return fail(PODP_ERR_ARG, "ctx is NULL");
+  if (F < 0) return fail(PODP_ERR_ARG, "F < 0");
+  if (F == 0) return PODP_OK;
+  if (!omega_d || !T1_d || !I_d || !Delta_d) return fail(PODP_ERR_ARG, "null omega/output pointer");
+  if ((flags & PODP_FLAG_OUT_P) && !P_d) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P set but P_d is NULL");
+  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
+  DeviceGuard guard(c->device);
+  if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  podp::EvalArgs a;
+  a.ops = c->d_ops;
+  a.L = c->L;
+  a.r = c->r;
+  a.n_obj = c->n_obj;
+  a.omega = omega_d;
+  a.F = F;
+  a.T1 = T1_d;
+  a.I = I_d;
+  a.Delta = Delta_d;
+  a.info = info_d;
+  a.P_out = (flags & PODP_FLAG_OUT_P) ? P_d : nullptr;
+  a.flags = flags;
+  a.Pws = nullptr;
+  const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
+  cudaError_t e = cudaMallocAsync((void **)&a.Pws, ws, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
+  int nl = 0;
+  e = podp::launch_solve(a, s, &nl);
+  if (e == cudaSuccess) e = podp::launch_mpt(a, s, &nl);
+  cudaFreeAsync(a.Pws, s);
+  g_last_launches = nl;
+  if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");
+  return PODP_OK;
+}
+
+podp_status podp_eval_host(const podp_ctx *c, const double *omega_h, int64_t F, double *T1_h, double *I_h,
+                           double *Delta_h, int32_t *info_h, int flags, void *cuda_stream) {
+  g_err.clear();
+  if (!c) return fail(PODP_ERR_ARG, "ctx is NULL");
+  if (F < 0) return fail(PODP_ERR_ARG, "F < 0");
+  if (F == 0) return PODP_OK;
+  if (!omega_h || !T1_h || !I_h || !Delta_h) return fail(PODP_ERR_ARG, "null omega/output pointer");
+  if (flags & PODP_FLAG_OUT_P) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P is not available on the host entry point");
+  DeviceGuard guard(c->device);
+  if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const size_t nout = (size_t)c->n_obj * F * 6;
+  const size_t bytes = sizeof(double) * (F + 3 * nout) + sizeof(int32_t) * (size_t)c->n_obj * F;
+  char *buf = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host eval staging)");
+  double *om = (double *)buf, *T1 = om + F, *I = T1 + nout, *D = I + nout;
+  int32_t *info = (int32_t *)(D + nout);
+  e = cudaMemcpyAsync(om, omega_h, sizeof(double) * F, cudaMemcpyHostToDevice, s);
+  podp_status st = PODP_OK;
+  if (e == cudaSuccess) {
+    st = podp_eval(c, om, F, T1, I, D, info_h ? info : nullptr, nullptr, flags, s);
+    if (st == PODP_OK) {
+      e = cudaMemcpyAsync(T1_h, T1, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(I_h, I, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(Delta_h, D, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess && info_h)
+        e = cudaMemcpyAsync(info_h, info, sizeof(int32_t) * c->n_obj * F, cudaMemcpyDeviceToHost, s);
+    }
+  }
+  cudaFreeAsync(buf, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (st != PODP_OK) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "podp_eval_host copies");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "podp_eval_host synchronize");
+  return PODP_OK;
+}
+
+podp_status podp_select(const podp_ctx *c, const double *omega_d, const double *Delta_d, int64_t F,
+                        const double *snap, int32_t n_snap, int32_t n_star, double theta, int32_t *n_new,
+                        double *omega_new, int64_t *idx_new, double *Lambda, double *Lambda_n, void *cuda_stream) {
+  g_err.clear();
+  g_last_launches = 0;
+  if (!c) return fail(PODP_ERR_ARG, "ctx is NULL");
+  if (F < 0 || (F > 0 && (!omega_d || !Delta_d))) return fail(PODP_ERR_ARG, "bad omega/Delta/F");
+  if (!snap || n_snap < 2 || n_snap > PODP_SNAP_MAX) return fail(PODP_ERR_ARG, "need 2 <= n_snap <= %d", PODP_SNAP_MAX);
+  for (int i = 0; i < n_snap; ++i) {
+    if (!std::isfinite(snap[i])) return fail(PODP_ERR_ARG, "snapshot %d is not finite", i);
+    if (i && !(snap[i] > snap[i - 1])) return fail(PODP_ERR_ARG, "snapshots must be strictly ascending");
+  }
+  if (n_star < 1 || n_star > 64) return fail(PODP_ERR_ARG, "need 1 <= n_star <= 64");
+  if (!(theta <= 1.0) || std::isnan(theta)) return fail(PODP_ERR_ARG, "theta must be <= 1 (<= 0 selects top-N* mode)");
+  if (!n_new || !omega_new || !idx_new || !Lambda) return fail(PODP_ERR_ARG, "null output pointer");
+  DeviceGuard guard(c->device);
+  if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int n_int = n_snap - 1;
+  const size_t n_res = 2 + n_int + 2 * (size_t)n_star;
+  const size_t bytes = sizeof(double) * (n_snap + n_res) + 2 * sizeof(unsigned long long) * n_int;
+  char *buf = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(select scratch)");
+  double *snap_d = (double *)buf, *res_d = snap_d + n_snap;
+  unsigned long long *keys = (unsigned long long *)(res_d + n_res), *args = keys + n_int;
+  std::vector<double> res(n_res);
+  int nl = 0;
+  e = cudaMemcpyAsync(snap_d, snap, sizeof(double) * n_snap, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = podp::launch_select(omega_d, Delta_d, F, snap_d, n_snap, n_star, theta, keys, args, res_d, s, &nl);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(res.data(), res_d, sizeof(double) * n_res, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  g_last_launches = nl;
+  if (e != cudaSuccess) return cuda_fail(e, "podp_select");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "podp_select synchronize");
+  if (Lambda_n)
+    for (int n = 0; n < n_int; ++n) Lambda_n[n] = res[2 + n];
+  *Lambda = res[1];
+  const int nc = (int)res[0];
+  if (nc < 0) {
+    *n_new = 0;
+    return fail(PODP_ERR_NO_CANDIDATES, "fewer non-empty intervals than requested");
+  }
+  *n_new = nc;
+  for (int q = 0; q < n_star; ++q) {
+    idx_new[q] = q < nc ? (int64_t)res[2 + n_int + q] : -1;
+    omega_new[q] = q < nc ? res[2 + n_int + n_star + q] : std::nan("");
+  }
+  return PODP_OK;
+}
+
+}  // extern "C"

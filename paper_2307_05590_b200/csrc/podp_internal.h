@@ -1,0 +1,47 @@
+// Internal declarations shared by the libpodp translation units (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "podp.h"
+
+namespace podp {
+
+// Packed per-object operator layout on the device (all doubles; complex = (re, im) pairs; row-major).
+// Built by podp_create (podp_api.cu) from the C-ABI inputs.  R = padded mode count (exact padding:
+// K_pad = diag(K, I), everything else zero-padded; SURVEY 7 "Padding r ... is exact").
+struct Layout {
+  int R;          // padded r
+  int64_t K, M, KR, Gkk, J, Gmm;  // R x R complex
+  int64_t b0, b1, H;              // 3 x R complex (direction-major: b0[c*R + i] = b0_user[i][c])
+  int64_t GbK, GbM;               // 6 x R complex (row a = b-slot a)
+  int64_t Gbb;                    // 6 x 6 complex
+  int64_t scal;                   // SCAL_N doubles (see below)
+  int64_t stride;                 // doubles per object (multiple of 32)
+};
+
+enum { SC_NU = 0, SC_ALPHA = 1, SC_ALPHA_LB = 2, SC_S = 4, SC_N0 = 13, SCAL_N = 32 };
+
+Layout make_layout(int R);
+
+struct EvalArgs {
+  const double *ops;   // packed operators, n_obj objects
+  Layout L;
+  int r;               // true r (for the P debug output)
+  int n_obj;
+  const double *omega; // F
+  int64_t F;
+  double *T1, *I, *Delta;
+  int32_t *info;
+  double *P_out;       // debug P (nullable)
+  double2 *Pws;        // workspace: n_obj x F x 3 x R complex (solve -> contraction hand-off)
+  int flags;
+};
+
+// Kernel launchers (return cudaGetLastError() after launch; count launches in *nlaunch).
+cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch);
+cudaError_t launch_mpt(const EvalArgs &a, cudaStream_t s, int *nlaunch);
+cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, const double *snap_d, int n_snap,
+                          int n_star, double theta, unsigned long long *lam_bits, unsigned long long *arg_idx,
+                          double *result_d, cudaStream_t s, int *nlaunch);
+
+}  // namespace podp

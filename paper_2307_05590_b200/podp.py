@@ -1,0 +1,223 @@
+"""Thin Python binding of libpodp's C ABI (include/podp.h) -- argument marshalling only.
+
+Every step of the on-line path (assembly, LU solve, MPT forms, certificate, selection) runs in the CUDA kernels
+of libpodp.so; this module only converts NumPy/PyTorch buffers into the pointers the ABI expects.  There is no
+CPU fallback: if libpodp.so is missing or a call fails, an exception is raised.
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpodp.so")
+
+PODP_OK = 0
+FLAG_DEFAULT = 0
+FLAG_OUT_R = 1 << 0
+FLAG_OUT_P = 1 << 1
+FLAG_NO_PIVOT = 1 << 2
+R_MAX = 128
+STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ERR_OOM", 4: "PODP_ERR_UNSUPPORTED",
+                5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}
+EXPORTED = ["podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
+            "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version"]
+
+
+class PodpError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class podp_operators(ctypes.Structure):
+    _fields_ = [("r", ctypes.c_int32), ("nu", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("alpha_lb", ctypes.c_double)] + [
+        (n, ctypes.POINTER(ctypes.c_double)) for n in ("K", "M", "K_R", "b0", "b1", "N0", "S", "H", "G")]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libpodp.so (in-tree).  Raises FileNotFoundError if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    i32, i64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    lib.podp_create.argtypes = [ctypes.POINTER(podp_operators), ctypes.c_int, P, ctypes.POINTER(P)]
+    lib.podp_create_batch.argtypes = [i32, ctypes.POINTER(podp_operators), ctypes.c_int, P, ctypes.POINTER(P)]
+    lib.podp_eval.argtypes = [P, P, i64, P, P, P, P, P, ctypes.c_int, P]
+    lib.podp_eval_host.argtypes = [P, P, i64, P, P, P, P, ctypes.c_int, P]
+    lib.podp_select.argtypes = [P, P, P, i64, P, i32, i32, dbl, P, P, P, P, P, P]
+    lib.podp_n_obj.argtypes = [P]
+    lib.podp_r.argtypes = [P]
+    lib.podp_destroy.argtypes = [P]
+    for fn in ("podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_destroy"):
+        getattr(lib, fn).restype = ctypes.c_int
+    lib.podp_n_obj.restype = i32
+    lib.podp_r.restype = i32
+    lib.podp_last_launch_count.restype = i32
+    lib.podp_last_error.restype = ctypes.c_char_p
+    lib.podp_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != PODP_OK:
+        raise PodpError(st, load_library().podp_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _c128(x, shape) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    if a.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _f64(x, shape) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if a.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {a.shape}")
+    return a
+
+
+def _marshal(o, keep: list) -> podp_operators:
+    """Duck-typed operator object (attributes K, M, K_R?, b0, b1, N0, S, H, G, nu, alpha, alpha_lb)."""
+    r = int(np.asarray(o.K).shape[0])
+    st = podp_operators()
+    st.r = r
+    st.nu, st.alpha, st.alpha_lb = float(o.nu), float(o.alpha), float(o.alpha_lb)
+    arrays = dict(K=_c128(o.K, (r, r)), M=_c128(o.M, (r, r)), b0=_c128(o.b0, (r, 3)), b1=_c128(o.b1, (r, 3)),
+                  N0=_f64(o.N0, (3, 3)), S=_f64(o.S, (3, 3)), H=_c128(o.H, (3, r)),
+                  G=_c128(o.G, (6 + 2 * r, 6 + 2 * r)))
+    kr = getattr(o, "K_R", None)
+    if kr is not None:
+        arrays["K_R"] = _c128(kr, (r, r))
+    for k, a in arrays.items():
+        keep.append(a)
+        setattr(st, k, _dptr(a))
+    return st
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Evaluator:
+    """podp_create / podp_create_batch + podp_eval / podp_eval_host / podp_select on one device."""
+
+    def __init__(self, ops, device: int = 0, stream=None):
+        lib = load_library()
+        ops_list = list(ops) if isinstance(ops, (list, tuple)) else [ops]
+        keep: list = []
+        arr = (podp_operators * len(ops_list))(*[_marshal(o, keep) for o in ops_list])
+        h = ctypes.c_void_p()
+        import torch
+        with torch.cuda.device(device):
+            _check(lib.podp_create_batch(len(ops_list), arr, device, _stream_handle(stream), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.n_obj = int(lib.podp_n_obj(h))
+        self.r = int(lib.podp_r(h))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().podp_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alloc_outputs(self, F: int, info: bool = True, want_P: bool = False):
+        import torch
+        dev = torch.device("cuda", self.device)
+        n = self.n_obj
+        out = dict(T1=torch.empty((n, F, 6), dtype=torch.float64, device=dev),
+                   I=torch.empty((n, F, 6), dtype=torch.float64, device=dev),
+                   Delta=torch.empty((n, F, 6), dtype=torch.float64, device=dev))
+        if info:
+            out["info"] = torch.empty((n, F), dtype=torch.int32, device=dev)
+        if want_P:
+            out["P"] = torch.empty((n, F, 3, self.r), dtype=torch.complex128, device=dev)
+        return out
+
+    def eval(self, omega, out: dict | None = None, flags: int = 0, info: bool = True, want_P: bool = False,
+             stream=None) -> dict:
+        """omega: 1-D float64 CUDA tensor (device-resident).  Asynchronous on `stream`."""
+        import torch
+        if not (isinstance(omega, torch.Tensor) and omega.is_cuda and omega.dtype == torch.float64 and omega.dim() == 1):
+            raise TypeError("omega must be a 1-D float64 CUDA tensor")
+        omega = omega.contiguous()
+        F = omega.shape[0]
+        if out is None:
+            out = self.alloc_outputs(F, info=info, want_P=want_P)
+        if want_P:
+            flags |= FLAG_OUT_P
+        lib = load_library()
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p()  # noqa: E731
+        _check(lib.podp_eval(self._h, p(omega), F, p(out["T1"]), p(out["I"]), p(out["Delta"]), p(out.get("info")),
+                             p(out.get("P")), flags, _stream_handle(stream)))
+        return out
+
+    def launches_last_call(self) -> int:
+        return int(load_library().podp_last_launch_count())
+
+    def eval_host(self, omega_h: np.ndarray, flags: int = 0, out: dict | None = None, stream=None) -> dict:
+        """End-to-end entry: host omega in, host outputs back (podp_eval_host; synchronises)."""
+        omega_h = np.ascontiguousarray(omega_h, dtype=np.float64)
+        F = omega_h.shape[0]
+        n = self.n_obj
+        if out is None:
+            out = dict(T1=np.empty((n, F, 6)), I=np.empty((n, F, 6)), Delta=np.empty((n, F, 6)),
+                       info=np.empty((n, F), dtype=np.int32))
+        lib = load_library()
+        vp = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p()  # noqa: E731
+        _check(lib.podp_eval_host(self._h, vp(omega_h), F, vp(out["T1"]), vp(out["I"]), vp(out["Delta"]),
+                                  vp(out.get("info")), flags, _stream_handle(stream)))
+        return out
+
+    def select(self, omega, Delta, snap, n_star: int = 2, theta: float = 0.0, stream=None):
+        """One Algorithm-1 selection step on device-resident omega (F) and Delta (F x 6) of one object."""
+        import torch
+        F = omega.shape[0]
+        if Delta.shape[-2:] != (F, 6) or not Delta.is_contiguous():
+            raise ValueError("Delta must be a contiguous F x 6 tensor")
+        snap = np.ascontiguousarray(snap, dtype=np.float64)
+        n_int = len(snap) - 1
+        n_new = ctypes.c_int32()
+        om_new = np.empty(n_star)
+        idx_new = np.empty(n_star, dtype=np.int64)
+        lam = ctypes.c_double()
+        lam_n = np.empty(max(n_int, 1))
+        lib = load_library()
+        _check(lib.podp_select(self._h, ctypes.c_void_p(omega.data_ptr()), ctypes.c_void_p(Delta.data_ptr()), F,
+                               ctypes.c_void_p(snap.ctypes.data), len(snap), n_star, float(theta),
+                               ctypes.byref(n_new), ctypes.c_void_p(om_new.ctypes.data),
+                               ctypes.c_void_p(idx_new.ctypes.data), ctypes.byref(lam),
+                               ctypes.c_void_p(lam_n.ctypes.data), _stream_handle(stream)))
+        k = n_new.value
+        return om_new[:k].copy(), idx_new[:k].copy(), lam.value, lam_n[:n_int].copy()

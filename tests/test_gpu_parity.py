@@ -1,0 +1,251 @@
+"""GPU-vs-oracle parity through the C ABI (SURVEY 8(c) metric, north_star tolerances: 1e-10 per tensor entry
+against the componentwise term magnitude, 1e-8 on Delta).  Marked gpu: run with `pytest -m gpu` on a B200."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.parity import TOL_DELTA, TOL_RI, errors
+from oracle.podp_oracle import solve_reduced
+import podp_inputs as g
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    return torch
+
+
+def run_gpu(torch, ops, omega, flags=None, want_P=False, device=0):
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    ev = Evaluator(ops, device=device)
+    w = torch.tensor(np.asarray(omega, dtype=np.float64), device=f"cuda:{device}")
+    out = ev.eval(w, flags=FLAG_OUT_R if flags is None else flags, want_P=want_P)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    ev.close()
+    return res
+
+
+def check_parity(ops, omega, res, obj=0, sample=None):
+    idx = range(len(omega)) if sample is None else sample
+    worst = np.zeros(3)
+    for f in idx:
+        w = float(omega[f])
+        o = oracle.evaluate_one(ops, w, out_R=True)
+        eR, eI, eD = errors(ops, w, res["T1"][obj, f], res["I"][obj, f], res["Delta"][obj, f],
+                            oracle.to6(o["R"]), oracle.to6(o["I"]), oracle.to6(o["Delta"]))
+        worst = np.maximum(worst, [eR.max(), eI.max(), eD.max()])
+    assert worst[0] <= TOL_RI, f"R parity {worst[0]:.3g}"
+    assert worst[1] <= TOL_RI, f"I parity {worst[1]:.3g}"
+    assert worst[2] <= TOL_DELTA, f"Delta parity {worst[2]:.3g}"
+    return worst
+
+
+def test_config0_full_parity_and_P(torch_cuda):
+    ops, ex = g.make_config0()
+    omega = g.omega_grid(200)
+    res = run_gpu(torch_cuda, ops, omega, want_P=True)
+    assert (res["info"] == 0).all()
+    check_parity(ops, omega, res)
+    for f in range(0, 200, 7):
+        Po = solve_reduced(ops.K, ops.M, ops.b0, ops.b1, ops.nu, float(omega[f]))
+        Pg = res["P"][0, f].T  # stored 3 x r
+        assert np.linalg.norm(Pg - Po) / np.linalg.norm(Po) <= 1e-10
+
+
+@pytest.mark.parametrize("r,F", [(24, 1000), (48, 333), (32, 257), (96, 61)])
+def test_config_generators_parity(torch_cuda, r, F):
+    ops = g.make_operators(r)
+    omega = g.omega_grid(F)
+    res = run_gpu(torch_cuda, ops, omega)
+    assert (res["info"] == 0).all()
+    check_parity(ops, omega, res)
+
+
+@pytest.mark.parametrize("r", [1, 2, 7, 33, 127, 128])
+def test_ragged_and_max_r(torch_cuda, r):
+    rng = np.random.default_rng(r)
+    if r % 2 == 0:
+        ops = g.make_operators(r, seed=r)
+    else:
+        base = g.make_operators(r + 1, seed=r)
+        # drop the last mode (still Hermitian / PSD); G keeps its structure via slot selection
+        keep = np.r_[0:6, 6:6 + r, 6 + r + 1:6 + 2 * r + 1]
+        ops = g.Operators(K=base.K[:r, :r], M=base.M[:r, :r], b0=base.b0[:r], b1=base.b1[:r], N0=np.eye(3),
+                          S=base.S, H=base.H[:, :r], G=base.G[np.ix_(keep, keep)], nu=base.nu, alpha=base.alpha,
+                          alpha_lb=base.alpha_lb)
+    omega = np.sort(10 ** rng.uniform(1, 8, 37))
+    res = run_gpu(torch_cuda, ops, omega)
+    check_parity(ops, omega, res)
+
+
+def test_default_flag_outputs_Rt(torch_cuda):
+    ops = g.make_operators(24)
+    ops.N0 = np.array([[1.0, 0.1, 0.0], [0.1, 2.0, 0.3], [0.0, 0.3, 3.0]])
+    omega = g.omega_grid(50)
+    a = run_gpu(torch_cuda, ops, omega, flags=0)
+    b = run_gpu(torch_cuda, ops, omega)
+    n06 = oracle.to6(ops.N0)
+    assert np.array_equal(a["T1"][0], n06[None, :] + b["T1"][0])
+    assert np.array_equal(a["I"], b["I"]) and np.array_equal(a["Delta"], b["Delta"])
+
+
+def test_no_pivot_flag_parity(torch_cuda):
+    from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_NO_PIVOT
+    ops = g.make_operators(48)
+    omega = g.omega_grid(97)
+    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_NO_PIVOT)
+    check_parity(ops, omega, res)
+
+
+def test_batch_objects_parity(torch_cuda):
+    sig = g.batch_sigma(256)
+    ops = [g.make_operators(32, seed=k, nu=g.MU0 * sig[k] * 1e-4) for k in range(5)]
+    omega = g.omega_grid(129)
+    res = run_gpu(torch_cuda, ops, omega)
+    assert res["T1"].shape == (5, 129, 6)
+    for k in range(5):
+        check_parity(ops[k], omega, res, obj=k, sample=range(0, 129, 4))
+
+
+def test_edge_cases_nonfinite_zero_F_singular(torch_cuda):
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    ops = g.make_operators(8)
+    omega = np.array([10.0, np.inf, 1e5, np.nan, 0.0, 1e8])
+    res = run_gpu(torch, ops, omega)
+    assert list(res["info"][0]) == [0, -1, 0, -1, 0, 0]
+    for f in (1, 3):
+        assert np.isnan(res["T1"][0, f]).all() and np.isnan(res["I"][0, f]).all() and np.isnan(res["Delta"][0, f]).all()
+    good = [0, 2, 4, 5]
+    check_parity(ops, omega, res, sample=good)
+    # F == 0 is a no-op
+    ev = Evaluator(ops)
+    out = ev.eval(torch.empty(0, dtype=torch.float64, device="cuda"))
+    assert out["T1"].shape == (1, 0, 6)
+    ev.close()
+    # exactly singular system: K = M = 0 -> zero pivot at step 0 -> info = 1 (LAPACK getrf convention)
+    z = g.Operators(**{**ops.__dict__, "K": np.zeros((8, 8), complex), "M": np.zeros((8, 8), complex)})
+    res = run_gpu(torch, z, np.array([1.0, 2.0]))
+    assert list(res["info"][0]) == [1, 1] and np.isnan(res["T1"]).all()
+
+
+def test_invariants_scaling_bitwise(torch_cuda):
+    """Remark 6.2, pin C8 on the GPU path: power-of-two scaling is exact -> bitwise."""
+    o = g.make_operators(24)
+    Dg = np.ones(6 + 2 * o.r)
+    Dg[[1, 3, 5]] = 4.0
+    o2 = g.Operators(**{**o.__dict__, "alpha": 2 * o.alpha, "nu": 4 * o.nu, "b1": 4 * o.b1, "S": 4 * o.S,
+                        "H": 4 * o.H, "G": (Dg[:, None] * o.G) * Dg[None, :]})
+    omega = g.omega_grid(64)
+    a = run_gpu(torch_cuda, o2, omega)
+    b = run_gpu(torch_cuda, o, 4 * omega)
+    for k in ("T1", "I", "Delta"):
+        assert np.array_equal(a[k], 8 * b[k]), k
+
+
+def test_symmetry_and_sign_structure_config0(torch_cuda):
+    ops, _ = g.make_config0()
+    omega = g.omega_grid(200)
+    res = run_gpu(torch_cuda, ops, omega)
+    for f in range(200):
+        R = oracle.from6(res["T1"][0, f])
+        I = oracle.from6(res["I"][0, f])
+        assert np.max(np.linalg.eigvalsh(R)) <= 1e-12 * np.abs(R).max()
+        assert np.min(np.linalg.eigvalsh(I)) >= -1e-12 * np.abs(I).max()
+        assert (res["Delta"][0, f] >= 0).all()
+
+
+def test_select_matches_oracle_on_gpu_delta(torch_cuda):
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator
+    ops = g.make_operators(24)
+    omega = g.omega_grid(20000)
+    snap = g.snapshot_grid(13)
+    ev = Evaluator(ops)
+    w = torch.tensor(omega, device="cuda")
+    out = ev.eval(w)
+    D = out["Delta"][0]
+    wn, idx, Lam, lam_n = ev.select(w, D, snap, n_star=2)
+    Dh = D.cpu().numpy()
+    ow, oidx, oLam, olam = oracle.select(omega, Dh, snap, 2)
+    assert list(idx) == oidx and list(wn) == ow and Lam == oLam
+    assert [x if x is not None else -1.0 for x in olam] == list(lam_n)
+    for theta in (1.0, 0.5, 1e-3):
+        wn, idx, Lam, _ = ev.select(w, D, snap, n_star=12, theta=theta)
+        ow, oidx, oLam, _ = oracle.select(omega, Dh, snap, 12, theta=theta)
+        assert list(idx) == oidx and Lam == oLam
+    # too many requested intervals -> PODP_ERR_NO_CANDIDATES
+    from paper_2307_05590_b200 import PodpError
+    with pytest.raises(PodpError) as ei:
+        ev.select(w, D, snap, n_star=13)
+    assert ei.value.status == 7
+    ev.close()
+
+
+def test_select_ties_and_nan(torch_cuda):
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator
+    ev = Evaluator(g.make_operators(8))
+    omega = np.linspace(1.0, 5.0, 4001)
+    snap = np.array([1.0, 2.0, 3.0, 4.0, 5.0])
+    D = np.zeros((4001, 6))
+    D[1500:1510, 2] = 7.0       # ties inside interval [2,3) -> lowest index 1500
+    D[2600, 0] = 7.0            # tie across intervals -> lower interval index wins for N*=1
+    D[100, 3] = np.nan
+    D[3000, :] = -0.0
+    wd, Dd = torch.tensor(omega, device="cuda"), torch.tensor(D, device="cuda")
+    wn, idx, Lam, lam_n = ev.select(wd, Dd, snap, n_star=1)
+    ow, oidx, oLam, _ = oracle.select(omega, D, snap, 1)
+    assert list(idx) == oidx == [1500] and Lam == oLam == 7.0
+    wn, idx, Lam, lam_n = ev.select(wd, Dd, snap, n_star=2)
+    assert list(idx) == oracle.select(omega, D, snap, 2)[1] == [1500, 2600]
+    ev.close()
+
+
+def test_eval_host_matches_device(torch_cuda):
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    ops = g.make_operators(48)
+    omega = g.omega_grid(1001)
+    ev = Evaluator(ops)
+    h = ev.eval_host(omega, flags=FLAG_OUT_R)
+    d = run_gpu(torch_cuda, ops, omega)
+    for k in ("T1", "I", "Delta", "info"):
+        assert np.array_equal(h[k], d[k]), k
+    ev.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_full_size_configs_sampled(torch_cuda, cfg):
+    """BASELINE configs at full size in the bench launch configuration; parity on a sample of outputs the
+    oracle computes one by one (plus properties that hold at any size)."""
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    c = g.make_config(cfg)
+    omega = c["omega"]
+    ev = Evaluator(c["ops"])
+    w = torch.tensor(omega, device="cuda")
+    out = ev.eval(w, flags=FLAG_OUT_R, info=True)
+    torch.cuda.synchronize()
+    F = len(omega)
+    rng = np.random.default_rng(cfg)
+    sample = sorted(set([0, F - 1, F // 2] + list(rng.integers(0, F, 40))))
+    n_obj = len(c["ops"])
+    objs = [0, n_obj - 1, n_obj // 2] if n_obj > 1 else [0]
+    for k in objs:
+        res = {key: out[key][k][sample].cpu().numpy()[None] for key in ("T1", "I", "Delta")}
+        check_parity(c["ops"][k], omega[sample], res)
+    assert int(out["info"].abs().sum()) == 0
+    assert torch.isfinite(out["Delta"]).all() and (out["Delta"] >= 0).all()
+    if cfg == 4:
+        wn, idx, Lam, lam_n = ev.select(w, out["Delta"][0], c["snap"], n_star=2)
+        ow, oidx, oLam, _ = oracle.select(omega, out["Delta"][0].cpu().numpy(), c["snap"], 2)
+        assert list(idx) == oidx and Lam == oLam
+    ev.close()
