@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "podp_internal.h"
 
@@ -258,7 +259,7 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   if (F == 0) return PODP_OK;
   if (!omega_d || !T1_d || !I_d || !Delta_d) return fail(PODP_ERR_ARG, "null omega/output pointer");
   if ((flags & PODP_FLAG_OUT_P) && !P_d) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P set but P_d is NULL");
-  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
+  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_INTERNAL_FORCE_GENERIC)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
   DeviceGuard guard(c->device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -276,14 +277,40 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   a.P_out = (flags & PODP_FLAG_OUT_P) ? P_d : nullptr;
   a.flags = flags;
   a.Pws = nullptr;
+  a.trace = nullptr;
+  static long long *trace_buf = nullptr;
+  if (getenv("PODP_LU_TRACE")) {
+    if (!trace_buf) cudaMallocManaged(&trace_buf, 8 * 1024 * sizeof(long long));
+    cudaMemset(trace_buf, 0, 8 * 1024 * sizeof(long long));
+    a.trace = trace_buf;
+  }
   const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
   cudaError_t e = cudaMallocAsync((void **)&a.Pws, ws, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
   int nl = 0;
-  e = podp::launch_solve(a, s, &nl);
+  e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_lu_reg(a, s);
+  if (e == cudaSuccess) {
+    ++nl;
+  } else if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    e = podp::launch_solve(a, s, &nl);
+  }
   if (e == cudaSuccess) e = podp::launch_mpt(a, s, &nl);
   cudaFreeAsync(a.Pws, s);
   g_last_launches = nl;
+  if (a.trace) {  // dev instrumentation dump (build with PODP_NVCC_EXTRA=-DPODP_LU_TRACE=1)
+    cudaDeviceSynchronize();
+    for (int q = 1; q < 3; ++q) {
+      const long long *tr = trace_buf + q * 1024;
+      if (!tr[0]) continue;
+      fprintf(stderr, "omega %d: LU end %lld, end %lld\n", q, tr[700] - tr[0], tr[708] - tr[0]);
+      for (int k = 0; k < 48; k += (k < 8 ? 1 : 8))
+        fprintf(stderr, "  step %2d: start %6lld %6lld %6lld %6lld | pass %6lld %6lld %6lld %6lld | srch %6lld redux %6lld shfl %6lld rcp %6lld end %6lld\n", k,
+                tr[k * 4 + 0] - tr[0], tr[k * 4 + 1] - tr[0], tr[k * 4 + 2] - tr[0], tr[k * 4 + 3] - tr[0],
+                tr[256 + k * 4 + 0] - tr[0], tr[256 + k * 4 + 1] - tr[0], tr[256 + k * 4 + 2] - tr[0], tr[256 + k * 4 + 3] - tr[0],
+                tr[512 + k] - tr[0], tr[640 + k + 1] - tr[0], tr[768 + k + 1] - tr[0], tr[832 + k + 1] - tr[0], tr[576 + k] - tr[0]);
+    }
+  }
   if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");
   return PODP_OK;
 }

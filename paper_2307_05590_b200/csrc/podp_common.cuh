@@ -29,6 +29,30 @@ __device__ __forceinline__ double2 crecip(double2 z) {
 }
 __device__ __forceinline__ double cabs1(double2 z) { return fabs(z.x) + fabs(z.y); }
 
+// 1/d for a normal, finite d > 0: hardware reciprocal seed (MUFU.RCP64H, ~2^-23) refined by two Newton steps
+// (relative error ~1 ulp).  Used on the LU pivot critical path instead of the IEEE division sequence (which adds
+// a slow-path branch and ~2x the latency).  Out-of-range d (|p| < 1e-150 or > 1e150) yields inf/0 and the
+// affected frequency is flagged non-finite downstream.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double2 crecip_fast(double2 z) {
+  const double inv = rcp_nr(fma(z.x, z.x, z.y * z.y));
+  return make_double2(z.x * inv, -z.y * inv);
+}
+// Pivot magnitude key: max(|Re|, |Im|) from the high words of the doubles (sign cleared), i.e. exponent + top
+// 20 mantissa bits, computed on the integer pipe.  Monotone in max(|Re|,|Im|) up to 2^-20 relative.
+__device__ __forceinline__ unsigned mag_key_hi(double2 z) {
+  const unsigned hr = (unsigned)(__double_as_longlong(z.x) >> 32) & 0x7FFFFFFFu;
+  const unsigned hi = (unsigned)(__double_as_longlong(z.y) >> 32) & 0x7FFFFFFFu;
+  return hr > hi ? hr : hi;
+}
+
 // Entry order of the 6 unique entries (11,22,33,12,13,23) -- SPEC S:355.
 __device__ __constant__ const int kPairI[6] = {0, 1, 2, 0, 0, 1};
 __device__ __constant__ const int kPairJ[6] = {0, 1, 2, 1, 2, 2};

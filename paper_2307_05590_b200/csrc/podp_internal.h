@@ -35,9 +35,14 @@ struct EvalArgs {
   double *P_out;       // debug P (nullable)
   double2 *Pws;        // workspace: n_obj x F x 3 x R complex (solve -> contraction hand-off)
   int flags;
+  long long *trace;    // dev instrumentation (nullable): clock64 stamps of block 0 / group 0
 };
 
 // Kernel launchers (return cudaGetLastError() after launch; count launches in *nlaunch).
+// Undocumented flag bit (testing only): force the generic shared-memory kernels.
+#define PODP_INTERNAL_FORCE_GENERIC (1 << 16)
+
+cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
 cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch);
 cudaError_t launch_mpt(const EvalArgs &a, cudaStream_t s, int *nlaunch);
 cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, const double *snap_d, int n_snap,

@@ -136,6 +136,26 @@ def test_edge_cases_nonfinite_zero_F_singular(torch_cuda):
     assert list(res["info"][0]) == [1, 1] and np.isnan(res["T1"]).all()
 
 
+@pytest.mark.parametrize("r", [24, 32, 48, 96])
+def test_edge_cases_fast_path(torch_cuda, r):
+    """Non-finite omega rows and an exactly singular system on the register-resident fast path."""
+    ops = g.make_operators(r)
+    omega = np.array([10.0, np.nan, 3e5, -np.inf, 1e8] + list(g.omega_grid(11)))
+    res = run_gpu(torch_cuda, ops, omega)
+    assert list(res["info"][0][:5]) == [0, -1, 0, -1, 0]
+    assert np.isnan(res["T1"][0, [1, 3]]).all() and np.isnan(res["Delta"][0, [1, 3]]).all()
+    check_parity(ops, omega, res, sample=[0, 2, 4] + list(range(5, 16)))
+    z = g.Operators(**{**ops.__dict__, "K": np.zeros((r, r), complex), "M": np.zeros((r, r), complex)})
+    res = run_gpu(torch_cuda, z, np.array([1.0, 2.0, 3.0]))
+    assert list(res["info"][0]) == [1, 1, 1] and np.isnan(res["I"]).all()
+    # singular at a later step: K = diag(1..r) with a zero at position 5, M = 0 -> zero pivot at step 5
+    d = np.arange(1.0, r + 1)
+    d[5] = 0.0
+    z = g.Operators(**{**ops.__dict__, "K": np.diag(d).astype(complex), "M": np.zeros((r, r), complex)})
+    res = run_gpu(torch_cuda, z, np.array([1.0, 2.0]))
+    assert list(res["info"][0]) == [6, 6]
+
+
 def test_invariants_scaling_bitwise(torch_cuda):
     """Remark 6.2, pin C8 on the GPU path: power-of-two scaling is exact -> bitwise."""
     o = g.make_operators(24)

@@ -41,6 +41,34 @@ __global__ void dmma_kernel(double *out, long iters) {
   if (s == 12345.0) out[0] = s;
 }
 
+// half the warps issue DFMA chains, half issue DMMA: do the two FP64 paths share one pipe?
+__global__ void mixed_kernel(double *out, long iters_f, long iters_m) {
+  const int warp = threadIdx.x >> 5;
+  if (warp & 1) {
+    double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+    double c[4][2] = {};
+    for (long i = 0; i < iters_m; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+    }
+    double s = 0;
+    for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+    if (s == 12345.0) out[0] = s;
+  } else {
+    double acc[8];
+    for (int c = 0; c < 8; ++c) acc[c] = threadIdx.x * 1e-9 + c;
+    for (long i = 0; i < iters_f; ++i) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fma(acc[c], 0.999999, 1e-7);
+    }
+    double s = 0;
+    for (int c = 0; c < 8; ++c) s += acc[c];
+    if (s == 12345.0) out[0] = s;
+  }
+}
+
 int main() {
   cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, 0));
   printf("{\"device\":\"%s\",\"sms\":%d,\"smem_per_block_optin\":%zu,\"regs_per_sm\":%d}\n",
@@ -73,6 +101,24 @@ int main() {
     }
     double flops = 2.0 * 256 * 4 * iters * (double)(threads / 32) * sms * blocks_per_sm;
     printf("{\"kind\":\"dmma_burst\",\"blocks_per_sm\":%d,\"ms\":%.3f,\"tflops\":%.3f}\n", blocks_per_sm, best, flops / best / 1e9);
+  }
+  {
+    // mixed: 4 blocks/SM x 256 threads; even warps DFMA (iters_f), odd warps DMMA (iters_m)
+    const int threads = 256, bps = 4;
+    const long iters_f = 20000, iters_m = 4000;
+    for (int mode = 0; mode < 1; ++mode) {
+      float best = 1e30f;
+      for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        mixed_kernel<<<sms * bps, threads>>>(out, iters_f, iters_m);
+        cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+      }
+      const double nw = (double)sms * bps * (threads / 32) / 2;  // warps of each kind
+      const double fl_f = 2.0 * 8 * iters_f * 32 * nw, fl_m = 2.0 * 256 * 4 * iters_m * nw;
+      printf("{\"kind\":\"mixed_dfma_dmma\",\"ms\":%.3f,\"tflops_total\":%.3f,\"tflops_dfma_part\":%.3f,\"tflops_dmma_part\":%.3f}\n",
+             best, (fl_f + fl_m) / best / 1e9, fl_f / best / 1e9, fl_m / best / 1e9);
+    }
   }
   // sustained: ~4 s of back-to-back launches
   for (int which = 0; which < 2; ++which) {
