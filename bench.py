@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the PODP on-line hot path on B200 -- prints ONE JSON line.
+
+Workload (BASELINE.json metric / configs[2]): r = 48 POD modes, F = 1e5 log-spaced output frequencies per GPU on
+[1e1, 1e8] rad/s, seeded synthetic operators (podp_inputs.make_operators, seed 0).  One "step" = one pass of the
+whole hot path over the F frequencies: podp_eval (shifted LU solve, MPT R/I, certificate Delta) + podp_select
+(one Algorithm-1 argmax step over the 13 log-spaced snapshot intervals).  podp_create (row a1, packing) is
+omega-independent and timed once, outside the steps.
+
+Multi-GPU (torchrun, one rank per GPU): frequencies shard with no data-path collective (weak scaling: each rank
+evaluates its own contiguous block of an N*F-point log grid); timing is the max over ranks.
+
+--impl reference runs the CPU oracle (oracle/, the slow plain NumPy implementation) on the box's host cores on
+a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPT frequencies/sec (3x3 R,I + error bound, FP64) at r=48; % FP64 peak"
+UNIT = "freq/s"
+R_HEAD = 48
+F_HEAD = 100_000
+# Measured FP64 peaks on this pool's B200 (tools/fp64_peak.cu, profiles/r01_fp64_peak.jsonl): DMMA (mma.sync f64)
+# 36.95 TF/s sustained, DFMA 34.0 TF/s; both paths share the FP64 units (mixed run: 36.8 TF/s total).
+FP64_PEAK_TFLOPS = 36.95
+
+
+def falg(r: int) -> float:
+    """Algorithmic FP64 flops per frequency: (8/3)r^3 + 107 r^2 + 190 r."""
+    return (8.0 / 3.0) * r ** 3 + 107.0 * r ** 2 + 190.0 * r
+
+
+def falg_solve(r: int) -> float:
+    """Flops of the solve kernel's share of F_alg: LU (8/3 r^3 - r^2) + 3-RHS solves (24 r^2) + A assembly (4 r^2)."""
+    return (8.0 / 3.0) * r ** 3 - r ** 2 + 24.0 * r ** 2 + 4.0 * r ** 2
+
+
+def falg_mpt(r: int) -> float:
+    """Flops of the MPT/certificate kernel's share: K_R P, M P, Q formation, Q P (80 r^2) + epilogues (~190 r)."""
+    return falg(r) - falg_solve(r)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sample(ops, omega, workers: int):
+    """Time the CPU oracle (as it stands) over `omega` on `workers` processes; returns (seconds, n)."""
+    import multiprocessing as mp
+    env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in env_keys}
+    for k in env_keys:
+        os.environ[k] = "1"
+    try:
+        chunks = [omega[i::workers] for i in range(workers)]
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(workers) as pool:
+            pool.map(_oracle_chunk, [(ops, omega[:2])] * workers)  # warm the workers (imports)
+            t0 = time.perf_counter()
+            pool.map(_oracle_chunk, [(ops, c) for c in chunks])
+            dt = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return dt, len(omega)
+
+
+def _oracle_chunk(args):
+    ops, om = args
+    import oracle
+    oracle.evaluate(ops, om, out_R=False)
+    return len(om)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int):
+    """--impl reference: the oracle on host cores (rank 0 only), bounded sample per step."""
+    if rank != 0:
+        return
+    import numpy as np
+    import podp_inputs as g
+    ops = g.make_operators(R_HEAD, seed=0)
+    omega_full = g.omega_grid(F_HEAD)
+    cores = host_cores()
+    n_per_step = int(os.environ.get("PODP_REF_SAMPLE", str(512 * cores)))
+    idx = np.linspace(0, F_HEAD - 1, n_per_step).astype(int)
+    sample = omega_full[idx]
+    for _ in range(args.warmup):
+        oracle_sample(ops, sample[: max(cores, 64)], cores)
+    tot, n = 0.0, 0
+    for _ in range(args.steps):
+        dt, k = oracle_sample(ops, sample, cores)
+        tot += dt
+        n += k
+    value = n / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2_r48_F1e5 (BASELINE configs[2]); oracle on a bounded evenly-spaced sample",
+                   "r": R_HEAD, "F_per_gpu": F_HEAD, "sample_per_step": n_per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{n_per_step} of the {F_HEAD} c2 frequencies (evenly spaced) per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="podp", choices=["podp", "reference"])
+    ap.add_argument("--F", type=int, default=F_HEAD)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    import numpy as np
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    import podp_inputs as g
+    import paper_2307_05590_b200 as pb
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    F = args.F
+    ops = g.make_operators(R_HEAD, seed=0)
+    # weak scaling: rank r owns block r of an (world*F)-point log grid on [1e1, 1e8]
+    omega_all = g.omega_grid(F * world)
+    omega_h = np.ascontiguousarray(omega_all[rank * F:(rank + 1) * F])
+    snap = g.snapshot_grid(13)
+    stream = torch.cuda.current_stream()
+
+    t0 = time.perf_counter()
+    ev = pb.Evaluator(ops, device=local)
+    torch.cuda.synchronize()
+    create_ms = (time.perf_counter() - t0) * 1e3
+
+    w_d = torch.tensor(omega_h, device=dev)
+    out = ev.alloc_outputs(F, info=True)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        ev.eval(w_d, out=out)
+        n = ev.launches_last_call()
+        ev.select(w_d, out["Delta"][0], snap, n_star=2)
+        return n + ev.launches_last_call()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    pb.profile_enable(True)
+    pb.profile_read(reset=True)
+    launches = 0
+    step_ms = []
+    with ClockSampler(local) as clk:
+        time.sleep(0.6)  # let nvidia-smi start sampling before the timed region
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (untimed)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launches += step()  # select synchronises the stream at its end
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    prof = pb.profile_read(reset=True)
+    pb.profile_enable(False)
+    total_ms = float(sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = (F * world * args.steps) / (total_ms / 1e3)
+
+    # end-to-end through the public host-buffer entry point (podp_eval_host): H2D omega, D2H outputs per step
+    T1h = torch.empty((1, F, 6), dtype=torch.float64, pin_memory=True).numpy()
+    Ih = torch.empty((1, F, 6), dtype=torch.float64, pin_memory=True).numpy()
+    Dh = torch.empty((1, F, 6), dtype=torch.float64, pin_memory=True).numpy()
+    infoh = torch.empty((1, F), dtype=torch.int32, pin_memory=True).numpy()
+    om_pin = torch.empty(F, dtype=torch.float64, pin_memory=True).numpy()
+    om_pin[:] = omega_h
+    hout = dict(T1=T1h, I=Ih, Delta=Dh, info=infoh)
+    for _ in range(2):
+        ev.eval_host(om_pin, out=hout)
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ev.eval_host(om_pin, out=hout)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = (F * world * args.steps) / (e2e_ms / 1e3)
+    h2d = omega_h.nbytes
+    d2h = T1h.nbytes + Ih.nbytes + Dh.nbytes + infoh.nbytes
+
+    if rank == 0:
+        solve_ms, solve_n = prof.get("solve", (0.0, 1))
+        mpt_ms, mpt_n = prof.get("mpt", (0.0, 1))
+        sel_ms, sel_n = prof.get("select", (0.0, 1))
+        dom = "solve" if solve_ms >= mpt_ms else "mpt"
+        dom_ms = (solve_ms / max(solve_n, 1)) if dom == "solve" else (mpt_ms / max(mpt_n, 1))
+        dom_flops = F * (falg_solve(R_HEAD) if dom == "solve" else falg_mpt(R_HEAD))
+        achieved = dom_flops / (dom_ms / 1e3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")
+            except (ValueError, OSError):
+                traffic = None
+        step_flops = F * falg(R_HEAD)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2_r48_F1e5 (BASELINE configs[2]): podp_eval + podp_select per step",
+                       "r": R_HEAD, "F_per_gpu": F, "omega": "logspace(1,8,N*F) block per rank",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "parallelism": f"dp{world} (independent omega shards, no data-path collective)",
+                       "podp_create_ms": round(create_ms, 3)},
+            "pct_fp64_peak": 100.0 * step_flops / (total_ms / args.steps / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+            "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": "measured FP64 (mma.sync f64 / DFMA share one pipe), tools/fp64_peak.cu",
+                         "flops_per_launch": dom_flops},
+            "kernel_ms_per_step": {k: v[0] / max(v[1], 1) * (v[1] / args.steps) for k, v in prof.items()},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+        }
+        line["clocks"] = clk.summary()
+        if not args.no_cpu_baseline:
+            cores = host_cores()
+            n_s = int(os.environ.get("PODP_CPU_SAMPLE", str(1024 * cores)))
+            idx = np.linspace(0, F - 1, n_s).astype(int)
+            dt, n = oracle_sample(ops, omega_h[idx], cores)
+            line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                    "sample": f"{n_s} evenly spaced of the {F} c2 frequencies ({dt:.1f} s)"}
+        print(json.dumps(line), flush=True)
+    ev.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

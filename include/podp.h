@@ -128,6 +128,14 @@ int32_t podp_r(const podp_ctx *ctx);
 /* Number of kernel launches the last podp_eval on this thread enqueued (bench bookkeeping). */
 int32_t podp_last_launch_count(void);
 
+/* Benchmark instrumentation.  While enabled (on != 0), podp_eval / podp_select record a CUDA event pair on the
+ * caller's stream around each kernel they launch ("solve", "mpt", "select").  podp_profile_read accumulates the
+ * elapsed time of every recorded pair per kernel name; call it only after the streams used are idle (it calls
+ * cudaEventSynchronize on each pair).  names: n x 32 chars (NUL-terminated), ms/counts: n entries.
+ * Returns the number of distinct names written (<= max_entries); reset != 0 clears the accumulators. */
+podp_status podp_profile_enable(int on);
+int32_t podp_profile_read(char *names, double *ms, int64_t *counts, int32_t max_entries, int32_t reset);
+
 /* Release a context (NULL-safe; synchronises the device work that used it is the caller's job). */
 podp_status podp_destroy(podp_ctx *ctx);
 

@@ -16,11 +16,38 @@ struct podp_ctx {
   int n_obj;
   podp::Layout L;
   double *d_ops;
+  cudaMemPool_t pool;  // stream-ordered scratch (P hand-off workspace, staging); keeps memory mapped between calls
 };
 
 namespace {
 
 thread_local std::string g_err;
+
+// ---- benchmark instrumentation (podp_profile_*) ---------------------------------------------------------------
+struct ProfPair {
+  const char *name;
+  cudaEvent_t a, b;
+};
+bool g_prof_on = false;
+std::vector<ProfPair> g_prof_pending;
+std::vector<std::pair<std::string, std::pair<double, int64_t>>> g_prof_acc;
+
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  const char *name;
+  cudaStream_t s;
+  ProfScope(const char *n, cudaStream_t st) : name(n), s(st) {
+    if (!g_prof_on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    g_prof_pending.push_back({name, a, b});
+  }
+};
 thread_local int g_last_launches = 0;
 
 podp_status fail(podp_status st, const char *fmt, ...) {
@@ -228,7 +255,23 @@ podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int devi
     cudaFree(d);
     return cuda_fail(e, "upload operators");
   }
+  cudaMemPool_t pool = nullptr;
+  {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    e = cudaMemPoolCreate(&pool, &pp);
+    if (e != cudaSuccess) {
+      cudaFree(d);
+      return cuda_fail(e, "cudaMemPoolCreate");
+    }
+    uint64_t thr = UINT64_MAX;  // never trim: the per-call workspace is re-used without re-mapping
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   podp_ctx *c = new podp_ctx;
+  c->pool = pool;
   c->device = device;
   c->r = r;
   c->n_obj = n_obj;
@@ -242,10 +285,49 @@ podp_status podp_create(const podp_operators *ops, int device, void *cuda_stream
   return podp_create_batch(1, ops, device, cuda_stream, out);
 }
 
+podp_status podp_profile_enable(int on) {
+  g_prof_on = on != 0;
+  return PODP_OK;
+}
+
+int32_t podp_profile_read(char *names, double *ms, int64_t *counts, int32_t max_entries, int32_t reset) {
+  for (auto &pp : g_prof_pending) {
+    float t = 0.f;
+    cudaEventSynchronize(pp.b);
+    cudaEventElapsedTime(&t, pp.a, pp.b);
+    cudaEventDestroy(pp.a);
+    cudaEventDestroy(pp.b);
+    bool found = false;
+    for (auto &acc : g_prof_acc)
+      if (acc.first == pp.name) {
+        acc.second.first += t;
+        acc.second.second += 1;
+        found = true;
+      }
+    if (!found) g_prof_acc.push_back({pp.name, {t, 1}});
+  }
+  g_prof_pending.clear();
+  int32_t n = 0;
+  for (auto &acc : g_prof_acc) {
+    if (n >= max_entries) break;
+    if (names) {
+      strncpy(names + 32 * n, acc.first.c_str(), 31);
+      names[32 * n + 31] = 0;
+    }
+    if (ms) ms[n] = acc.second.first;
+    if (counts) counts[n] = acc.second.second;
+    ++n;
+  }
+  if (reset) g_prof_acc.clear();
+  return n;
+}
+
 podp_status podp_destroy(podp_ctx *c) {
   if (!c) return PODP_OK;
   DeviceGuard guard(c->device);
+  cudaDeviceSynchronize();
   cudaFree(c->d_ops);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
   return PODP_OK;
 }
@@ -285,17 +367,23 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
     a.trace = trace_buf;
   }
   const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
-  cudaError_t e = cudaMallocAsync((void **)&a.Pws, ws, s);
+  cudaError_t e = cudaMallocFromPoolAsync((void **)&a.Pws, ws, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
   int nl = 0;
-  e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_lu_reg(a, s);
-  if (e == cudaSuccess) {
-    ++nl;
-  } else if (e == cudaErrorNotSupported) {
-    cudaGetLastError();
-    e = podp::launch_solve(a, s, &nl);
+  {
+    ProfScope ps("solve", s);
+    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_lu_reg(a, s);
+    if (e == cudaSuccess) {
+      ++nl;
+    } else if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = podp::launch_solve(a, s, &nl);
+    }
   }
-  if (e == cudaSuccess) e = podp::launch_mpt(a, s, &nl);
+  if (e == cudaSuccess) {
+    ProfScope ps("mpt", s);
+    e = podp::launch_mpt(a, s, &nl);
+  }
   cudaFreeAsync(a.Pws, s);
   g_last_launches = nl;
   if (a.trace) {  // dev instrumentation dump (build with PODP_NVCC_EXTRA=-DPODP_LU_TRACE=1)
@@ -329,7 +417,7 @@ podp_status podp_eval_host(const podp_ctx *c, const double *omega_h, int64_t F, 
   const size_t nout = (size_t)c->n_obj * F * 6;
   const size_t bytes = sizeof(double) * (F + 3 * nout) + sizeof(int32_t) * (size_t)c->n_obj * F;
   char *buf = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+  cudaError_t e = cudaMallocFromPoolAsync((void **)&buf, bytes, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host eval staging)");
   double *om = (double *)buf, *T1 = om + F, *I = T1 + nout, *D = I + nout;
   int32_t *info = (int32_t *)(D + nout);
@@ -375,14 +463,17 @@ podp_status podp_select(const podp_ctx *c, const double *omega_d, const double *
   const size_t n_res = 2 + n_int + 2 * (size_t)n_star;
   const size_t bytes = sizeof(double) * (n_snap + n_res) + 2 * sizeof(unsigned long long) * n_int;
   char *buf = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+  cudaError_t e = cudaMallocFromPoolAsync((void **)&buf, bytes, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(select scratch)");
   double *snap_d = (double *)buf, *res_d = snap_d + n_snap;
   unsigned long long *keys = (unsigned long long *)(res_d + n_res), *args = keys + n_int;
   std::vector<double> res(n_res);
   int nl = 0;
   e = cudaMemcpyAsync(snap_d, snap, sizeof(double) * n_snap, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = podp::launch_select(omega_d, Delta_d, F, snap_d, n_snap, n_star, theta, keys, args, res_d, s, &nl);
+  if (e == cudaSuccess) {
+    ProfScope ps("select", s);
+    e = podp::launch_select(omega_d, Delta_d, F, snap_d, n_snap, n_star, theta, keys, args, res_d, s, &nl);
+  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(res.data(), res_d, sizeof(double) * n_res, cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(buf, s);
   cudaError_t e2 = cudaStreamSynchronize(s);

@@ -24,7 +24,8 @@ R_MAX = 128
 STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ERR_OOM", 4: "PODP_ERR_UNSUPPORTED",
                 5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}
 EXPORTED = ["podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
-            "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version"]
+            "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version", "podp_profile_enable",
+            "podp_profile_read"]
 
 
 class PodpError(RuntimeError):
@@ -67,9 +68,33 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.podp_r.restype = i32
     lib.podp_last_launch_count.restype = i32
     lib.podp_last_error.restype = ctypes.c_char_p
+    lib.podp_profile_enable.argtypes = [ctypes.c_int]
+    lib.podp_profile_enable.restype = ctypes.c_int
+    lib.podp_profile_read.argtypes = [P, P, P, i32, i32]
+    lib.podp_profile_read.restype = i32
     lib.podp_version.restype = ctypes.c_char_p
     _lib = lib
     return lib
+
+
+def profile_enable(on: bool = True):
+    """Record CUDA event pairs around each libpodp kernel launch (bench instrumentation)."""
+    load_library().podp_profile_enable(1 if on else 0)
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{kernel name: (total ms, launches)} accumulated since the last reset; call when streams are idle."""
+    lib = load_library()
+    n_max = 16
+    names = ctypes.create_string_buffer(32 * n_max)
+    ms = np.zeros(n_max)
+    cnt = np.zeros(n_max, dtype=np.int64)
+    n = lib.podp_profile_read(names, ms.ctypes.data, cnt.ctypes.data, n_max, 1 if reset else 0)
+    out = {}
+    for i in range(n):
+        nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def _check(st: int):
