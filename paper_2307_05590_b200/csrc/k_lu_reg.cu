@@ -59,7 +59,7 @@ using IC = std::integral_constant<int, N>;
 
 }  // namespace lureg
 
-template <int R, int NW, int GPB>
+template <int R, int NW, int GPB, bool PIV = true>
 __global__ void __launch_bounds__(NW * 32 * GPB, 1) lu_reg_kernel(EvalArgs a) {
   using C = lureg::Cfg<R, NW, GPB>;
   constexpr int NCOL = C::NCOL, MR = C::MR, NC = C::NC, LDKM = C::LDKM, CP = C::CP;
@@ -136,18 +136,25 @@ __global__ void __launch_bounds__(NW * 32 * GPB, 1) lu_reg_kernel(EvalArgs a) {
       auto search = [&](auto kn_c) __attribute__((always_inline)) {
         constexpr int KN = decltype(kn_c)::value;
         constexpr int GK = (KN / NW) & 1, NK = KN / CP, MKN = KN >> 4, RKN = KN & 15;
-        unsigned key = 0u;
+        unsigned best;
+        int p;
+        if constexpr (PIV) {
+          unsigned key = 0u;
 #pragma unroll
-        for (int m = 0; m < MR; ++m) {
-          if (16 * m + 15 >= KN && 16 * m < R) {
-            const int i = rho + 16 * m;
-            const unsigned kk = (mag_key_hi(A[m][NK]) & 0xFFFFFF80u) | (unsigned)(127 - i);
-            const bool cand = gam == GK && i >= KN && i < R;
-            key = (cand && kk > key) ? kk : key;
+          for (int m = 0; m < MR; ++m) {
+            if (16 * m + 15 >= KN && 16 * m < R) {
+              const int i = rho + 16 * m;
+              const unsigned kk = (mag_key_hi(A[m][NK]) & 0xFFFFFF80u) | (unsigned)(127 - i);
+              const bool cand = gam == GK && i >= KN && i < R;
+              key = (cand && kk > key) ? kk : key;
+            }
           }
+          best = __reduce_max_sync(0xffffffffu, key);
+          p = 127 - (int)(best & 127u);
+        } else {
+          p = KN;
+          best = 0xFFFFFFFFu;
         }
-        const unsigned best = __reduce_max_sync(0xffffffffu, key);
-        const int p = 127 - (int)(best & 127u);
         LU_TR(640 + KN);
         const int mp = p >> 4, rp = p & 15;
         double2 pv = A[MKN][NK];
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(NW * 32 * GPB, 1) lu_reg_kernel(EvalArgs a) {
         double2 dv;
         dv.x = __shfl_sync(0xffffffffu, A[MKN][NK].x, RKN + 16 * GK);
         dv.y = __shfl_sync(0xffffffffu, A[MKN][NK].y, RKN + 16 * GK);
-        const bool singular = (best >> 7) == 0u;
+        const bool singular = PIV ? (best >> 7) == 0u : (pv.x == 0.0 && pv.y == 0.0);
         LU_TR(768 + KN);
         if (!singular) {
           const double2 rc = crecip_fast(pv);
@@ -194,8 +201,9 @@ __global__ void __launch_bounds__(NW * 32 * GPB, 1) lu_reg_kernel(EvalArgs a) {
           __syncwarp();
         }
         LU_TR(256 + K * 4 + w);
-        const int p = sPiv[K & 1];
-        if (p < 0 && bad == 0) bad = K + 1;
+        const int p_raw = sPiv[K & 1];
+        if (p_raw < 0 && bad == 0) bad = K + 1;
+        const int p = PIV ? p_raw : K;
         constexpr bool HAS_NEXT = K + 1 < R;
         constexpr int K1 = K + 1, W1 = K1 % NW, NK1 = K1 / CP;
         const bool producer = HAS_NEXT && w == W1;
@@ -386,10 +394,10 @@ __global__ void __launch_bounds__(NW * 32 * GPB, 1) lu_reg_kernel(EvalArgs a) {
   }
 }
 
-template <int R, int NW, int GPB>
+template <int R, int NW, int GPB, bool PIV = true>
 static cudaError_t launch_lu_reg_t(const EvalArgs &a, cudaStream_t s) {
   using C = lureg::Cfg<R, NW, GPB>;
-  auto kern = lu_reg_kernel<R, NW, GPB>;
+  auto kern = lu_reg_kernel<R, NW, GPB, PIV>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -404,7 +412,10 @@ static cudaError_t launch_lu_reg_t(const EvalArgs &a, cudaStream_t s) {
 
 // Returns cudaErrorNotSupported when no register-resident instantiation exists for this R / flags.
 cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s) {
-  if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
+  if (a.flags & PODP_FLAG_NO_PIVOT) {
+    if (a.L.R == 48) return launch_lu_reg_t<48, 4, 4, false>(a, s);
+    return cudaErrorNotSupported;
+  }
   const char *v = getenv("PODP_LU_VARIANT");
   const int var = v ? atoi(v) : 0;
   switch (a.L.R) {

@@ -1,0 +1,264 @@
+// K3 fast path: MPT quadratic forms + error certificate, rows a4-a6 (see k_mpt.cu for the formulas / citations).
+//
+//   For every frequency and every pair i <= j:  Re(p_i^H K_R p_j), Re(p_i^H M p_j), Re(p_i^H Q(omega) p_j) with
+//   Q = G_KK + s J + s^2 G_MM formed on the fly (Horner, 4 DFMA per element), plus Re(l_i p_j), Re(h_i p_j).
+//
+// Layout.  Operator-stationary: the five r x r operators (K_R, M, G_KK, J, G_MM) live in shared memory (row
+// blocks of RB rows when they do not fit).  A warp owns 4 frequencies; lane = 8*f + s holds the b-slice
+// {b = s + 8t} of its frequency's P (3 columns) in registers.  For each operator row a, the lane forms its partial
+// y_j[a] = sum_{b in slice} Op[a][b] p_j[b] (all 8 lanes of a frequency read the same 8 consecutive operator
+// entries: one conflict-free wavefront per load) and immediately contracts it with conj(p_i[a]) into 18 running
+// sums; the 8 partial sums of a frequency are reduced by shuffles once per tile.  FP64 throughout.
+#include "podp_common.cuh"
+
+namespace podp {
+
+namespace mpttile {
+
+constexpr int WARPS = 8;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+template <int R>
+struct Cfg {
+  static constexpr int SL = R <= 64 ? 8 : 16;    // b-slices (lanes) per frequency
+  static constexpr int FPW = 32 / SL;             // frequencies per warp
+  static constexpr int TILE = WARPS * FPW;        // frequencies per CTA tile
+  static constexpr int NBL = (R + SL - 1) / SL;  // b's per lane
+  static constexpr int LD = R;                    // row stride (complex); 8 consecutive b's = 128 B
+  static constexpr int RB_MAX = SMEM_BUDGET / (5 * R * 16);
+  static constexpr int RB = RB_MAX >= R ? R : RB_MAX;  // rows per operator block
+  static constexpr int NBLK = (R + RB - 1) / RB;
+  static constexpr size_t BYTES = (size_t)5 * RB * LD * sizeof(double2);
+};
+
+}  // namespace mpttile
+
+template <int R>
+__global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalArgs a) {
+  using C = mpttile::Cfg<R>;
+  constexpr int NBL = C::NBL, RB = C::RB, NBLK = C::NBLK, LD = C::LD, SL = C::SL, TILE = C::TILE, FPW = C::FPW;
+  extern __shared__ double2 smem[];
+  double2 *sKR = smem, *sM = sKR + RB * LD, *sGk = sM + RB * LD, *sJ = sGk + RB * LD, *sGm = sJ + RB * LD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fl = lane / SL, sl = lane % SL;
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  const int64_t ntiles = (total + TILE - 1) / TILE;
+  int loaded_obj = -1;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = tile * TILE;
+    int64_t t = t0 + warp * FPW + fl;  // my frequency (global evaluation index)
+    const bool valid = t < total;
+    if (!valid) t = total - 1;
+    const int obj = (int)(t / a.F);
+    const int obj0 = (int)(t0 / a.F);
+    const int64_t tl = (t0 + TILE - 1 < total ? t0 + TILE - 1 : total - 1);
+    const bool one_obj = obj0 == (int)(tl / a.F);  // whole tile belongs to one object
+    const int64_t f = t - (int64_t)obj * a.F;
+    const double *op = a.ops + (size_t)obj * a.L.stride;
+    const double w = a.omega[f];
+    const double nu = op[a.L.scal + SC_NU];
+    const double s = w * nu;
+    // my slice of P (3 columns) into registers
+    const double2 *Pw = a.Pws + (size_t)t * 3 * R;
+    double2 p[NBL][3];
+#pragma unroll
+    for (int tt = 0; tt < NBL; ++tt) {
+      const int b = sl + SL * tt;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) p[tt][c] = (b < R) ? Pw[c * R + b] : make_double2(0.0, 0.0);
+    }
+    double qK[6], qM[6], qQ[6], lp[9], hp[9];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) qK[e] = qM[e] = qQ[e] = 0.0;
+    // linear terms over my slice: Re(l_i[b] p_j[b]), Re(h_i[b] p_j[b])
+    {
+      const double2 *GbK = reinterpret_cast<const double2 *>(op + a.L.GbK);
+      const double2 *GbM = reinterpret_cast<const double2 *>(op + a.L.GbM);
+      const double2 *H = reinterpret_cast<const double2 *>(op + a.L.H);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) lp[e] = hp[e] = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < NBL; ++tt) {
+        const int b = sl + SL * tt;
+        if (b < R) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const double2 k0 = __ldg(GbK + (2 * i) * R + b), k1 = __ldg(GbK + (2 * i + 1) * R + b);
+            const double2 m0 = __ldg(GbM + (2 * i) * R + b), m1 = __ldg(GbM + (2 * i + 1) * R + b);
+            const double2 gk = make_double2(fma(w, k1.x, k0.x), fma(w, k1.y, k0.y));
+            const double2 gm = make_double2(fma(w, m1.x, m0.x), fma(w, m1.y, m0.y));
+            const double2 l = make_double2(-gk.x + s * gm.y, -gk.y - s * gm.x);
+            const double2 h = __ldg(H + i * R + b);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              lp[i * 3 + j] = fma(l.x, p[tt][j].x, fma(-l.y, p[tt][j].y, lp[i * 3 + j]));
+              hp[i * 3 + j] = fma(h.x, p[tt][j].x, fma(-h.y, p[tt][j].y, hp[i * 3 + j]));
+            }
+          }
+        }
+      }
+    }
+    // quadratic forms, operator rows in blocks
+#pragma unroll 1
+    for (int blk = 0; blk < NBLK; ++blk) {
+      const int a0 = blk * RB, a1 = (a0 + RB < R) ? a0 + RB : R;
+      const bool need_load = one_obj && (NBLK > 1 || loaded_obj != obj0);  // CTA-uniform
+      if (need_load) {
+        __syncthreads();
+        const double *opl = a.ops + (size_t)obj0 * a.L.stride;
+        const double2 *gKR = reinterpret_cast<const double2 *>(opl + a.L.KR);
+        const double2 *gM = reinterpret_cast<const double2 *>(opl + a.L.M);
+        const double2 *gGk = reinterpret_cast<const double2 *>(opl + a.L.Gkk);
+        const double2 *gJ = reinterpret_cast<const double2 *>(opl + a.L.J);
+        const double2 *gGm = reinterpret_cast<const double2 *>(opl + a.L.Gmm);
+        const int n = (a1 - a0) * R;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) {
+          const int row = e / R, col = e - row * R;
+          const int src = (a0 + row) * R + col, dst = row * LD + col;
+          sKR[dst] = gKR[src];
+          sM[dst] = gM[src];
+          sGk[dst] = gGk[src];
+          sJ[dst] = gJ[src];
+          sGm[dst] = gGm[src];
+        }
+        __syncthreads();
+        loaded_obj = NBLK == 1 ? obj0 : -1;
+      }
+      // operators for this frequency: shared-memory block (tile of one object) or global (mixed tile)
+      const bool shared_ops = one_obj;
+      const double2 *oKR = shared_ops ? sKR : reinterpret_cast<const double2 *>(op + a.L.KR) + a0 * R;
+      const double2 *oM = shared_ops ? sM : reinterpret_cast<const double2 *>(op + a.L.M) + a0 * R;
+      const double2 *oGk = shared_ops ? sGk : reinterpret_cast<const double2 *>(op + a.L.Gkk) + a0 * R;
+      const double2 *oJ = shared_ops ? sJ : reinterpret_cast<const double2 *>(op + a.L.J) + a0 * R;
+      const double2 *oGm = shared_ops ? sGm : reinterpret_cast<const double2 *>(op + a.L.Gmm) + a0 * R;
+      const int ld = shared_ops ? LD : R;
+#pragma unroll 1
+      for (int ar = a0; ar < a1; ++ar) {
+        const int row = (ar - a0) * ld;
+        double2 pa[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pa[c] = __ldg(Pw + c * R + ar);
+        double2 yK[3], yM[3], yQ[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) yK[c] = yM[c] = yQ[c] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int tt = 0; tt < NBL; ++tt) {
+          const int b = sl + SL * tt;
+          if ((R % SL) == 0 || b < R) {
+            const double2 kr = oKR[row + b], mm = oM[row + b];
+            const double2 gk = oGk[row + b], jj = oJ[row + b], gm = oGm[row + b];
+            const double2 q = make_double2(fma(s, fma(s, gm.x, jj.x), gk.x), fma(s, fma(s, gm.y, jj.y), gk.y));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              yK[c] = cfma(kr, p[tt][c], yK[c]);
+              yM[c] = cfma(mm, p[tt][c], yM[c]);
+              yQ[c] = cfma(q, p[tt][c], yQ[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+          const int i = e < 3 ? e : (e < 5 ? 0 : 1);
+          const int j = e < 3 ? e : (e == 3 ? 1 : 2);
+          qK[e] = fma(pa[i].x, yK[j].x, fma(pa[i].y, yK[j].y, qK[e]));
+          qM[e] = fma(pa[i].x, yM[j].x, fma(pa[i].y, yM[j].y, qM[e]));
+          qQ[e] = fma(pa[i].x, yQ[j].x, fma(pa[i].y, yQ[j].y, qQ[e]));
+        }
+      }
+    }
+    // reduce the SL partial sums of each frequency (lanes SL*f .. SL*f+SL-1)
+#pragma unroll
+    for (int o = 1; o < SL; o <<= 1) {
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        qK[e] += __shfl_xor_sync(0xffffffffu, qK[e], o);
+        qM[e] += __shfl_xor_sync(0xffffffffu, qM[e], o);
+        qQ[e] += __shfl_xor_sync(0xffffffffu, qQ[e], o);
+      }
+#pragma unroll
+      for (int e = 0; e < 9; ++e) {
+        lp[e] += __shfl_xor_sync(0xffffffffu, lp[e], o);
+        hp[e] += __shfl_xor_sync(0xffffffffu, hp[e], o);
+      }
+    }
+    if (valid && sl == 0) {
+      double *T1 = a.T1 + (size_t)t * 6, *I = a.I + (size_t)t * 6, *D = a.Delta + (size_t)t * 6;
+      bool ok = isfinite(w);
+#pragma unroll
+      for (int e = 0; e < 6; ++e) ok &= isfinite(qK[e]) && isfinite(qM[e]) && isfinite(qQ[e]);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) ok &= isfinite(lp[e]) && isfinite(hp[e]);
+      if (!ok) {
+#pragma unroll
+        for (int e = 0; e < 6; ++e) T1[e] = I[e] = D[e] = nanv;
+      } else {
+        // epilogue (same arithmetic as mpt_epilogue in k_mpt.cu)
+        const double *sc = op + a.L.scal;
+        const double alpha = sc[SC_ALPHA], alb = sc[SC_ALPHA_LB];
+        const double a3 = alpha * alpha * alpha;
+        const double2 *Gbb = reinterpret_cast<const double2 *>(op + a.L.Gbb);
+        double ReX[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double g00 = Gbb[(2 * i) * 6 + 2 * j].x, g01 = Gbb[(2 * i) * 6 + 2 * j + 1].x;
+            const double g10 = Gbb[(2 * i + 1) * 6 + 2 * j].x, g11 = Gbb[(2 * i + 1) * 6 + 2 * j + 1].x;
+            const double c = g00 + w * (g01 + g10) + w * w * g11;
+            ReX[i * 3 + j] = c + lp[i * 3 + j] + lp[j * 3 + i];
+          }
+        double n[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const double x = ReX[i * 3 + i] + qQ[i];
+          n[i] = x > 0.0 ? x : 0.0;
+        }
+        const bool outR = a.flags & PODP_FLAG_OUT_R;
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+          const int i = e < 3 ? e : (e < 5 ? 0 : 1);
+          const int j = e < 3 ? e : (e == 3 ? 1 : 2);
+          const double Rv = -(a3 / 4.0) * qK[e];
+          T1[e] = outR ? Rv : sc[SC_N0 + 3 * i + j] + Rv;
+          I[e] = (w * a3 / 4.0) * (sc[SC_S + 3 * i + j] + nu * qM[e] + hp[i * 3 + j] + hp[j * 3 + i]);
+          double mij = 0.0;
+          if (i != j) {
+            const double x = n[i] + n[j] - 2.0 * (ReX[i * 3 + j] + qQ[e]);
+            mij = x > 0.0 ? x : 0.0;
+          }
+          D[e] = a3 / (8.0 * alb) * (n[i] + n[j] + mij);
+        }
+      }
+    }
+  }
+}
+
+template <int R>
+static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s) {
+  using C = mpttile::Cfg<R>;
+  auto kern = mpt_tile_kernel<R>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  int64_t blocks = (total + C::TILE - 1) / C::TILE;
+  if (blocks > sms) blocks = sms;
+  kern<<<(unsigned)blocks, mpttile::WARPS * 32, C::BYTES, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s) {
+  switch (a.L.R) {
+    case 24: return launch_mpt_tile_t<24>(a, s);
+    case 32: return launch_mpt_tile_t<32>(a, s);
+    case 48: return launch_mpt_tile_t<48>(a, s);
+    case 96: return launch_mpt_tile_t<96>(a, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace podp

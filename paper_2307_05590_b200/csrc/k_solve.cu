@@ -8,13 +8,15 @@
 
 namespace podp {
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) solve_smem_kernel(EvalArgs a) {
+// GLOBAL = true keeps [A | B] in a per-warp global-memory scratch (L1/L2 cached) instead of shared memory: the
+// fallback for R too large for a warp's shared-memory slice (R > ~118).
+template <int NW, bool GLOBAL>
+__global__ void __launch_bounds__(NW * 32) solve_smem_kernel(EvalArgs a, double2 *gscratch) {
   extern __shared__ double2 smem[];
   const int R = a.L.R;
   const int LD = R + 4;  // R + 3 columns, +1 pad
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2 *A = smem + (size_t)warp * R * LD;
+  double2 *A = GLOBAL ? gscratch + ((size_t)blockIdx.x * NW + warp) * R * LD : smem + (size_t)warp * R * LD;
   const int64_t total = (int64_t)a.n_obj * a.F;
   const bool pivot = !(a.flags & PODP_FLAG_NO_PIVOT);
 
@@ -112,9 +114,25 @@ __global__ void __launch_bounds__(NW * 32) solve_smem_kernel(EvalArgs a) {
   }
 }
 
-cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch) {
+size_t solve_scratch_bytes(int R, int sms) {
+  const size_t per_warp = (size_t)R * (R + 4) * sizeof(double2);
+  return per_warp > 200 * 1024 ? per_warp * (size_t)sms * 4 : 0;
+}
+
+cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch) {
   const int R = a.L.R;
   const size_t per_warp = (size_t)R * (R + 4) * sizeof(double2);
+  int dev0 = 0, sms0 = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  if (per_warp > 200 * 1024) {  // global-memory scratch fallback: one warp per block, 4 blocks per SM
+    if (!gscratch) return cudaErrorInvalidValue;
+    const int64_t total = (int64_t)a.n_obj * a.F;
+    int64_t blocks = total < (int64_t)sms0 * 4 ? total : (int64_t)sms0 * 4;
+    solve_smem_kernel<1, true><<<(unsigned)blocks, 32, 0, s>>>(a, gscratch);
+    ++*nlaunch;
+    return cudaGetLastError();
+  }
   int nw = (int)((200 * 1024) / per_warp);
   if (nw > 8) nw = 8;
   if (nw < 1) nw = 1;
@@ -126,12 +144,12 @@ cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch) {
 #define PODP_LAUNCH_SOLVE(NWv)                                                                              \
   {                                                                                                         \
     const size_t sm = per_warp * NWv;                                                                       \
-    e = cudaFuncSetAttribute(solve_smem_kernel<NWv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    e = cudaFuncSetAttribute(solve_smem_kernel<NWv, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     if (e != cudaSuccess) return e;                                                                         \
     int64_t blocks = (total + NWv - 1) / NWv;                                                               \
     int64_t cap = (int64_t)sms * 8;                                                                         \
     if (blocks > cap) blocks = cap;                                                                         \
-    solve_smem_kernel<NWv><<<(unsigned)blocks, NWv * 32, sm, s>>>(a);                                       \
+    solve_smem_kernel<NWv, false><<<(unsigned)blocks, NWv * 32, sm, s>>>(a, nullptr);                       \
   }
   if (nw >= 8) PODP_LAUNCH_SOLVE(8)
   else if (nw >= 4) PODP_LAUNCH_SOLVE(4)

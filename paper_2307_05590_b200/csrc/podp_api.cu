@@ -372,17 +372,33 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   int nl = 0;
   {
     ProfScope ps("solve", s);
-    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_lu_reg(a, s);
+    const char *lv = getenv("PODP_LU_IMPL");  // dev switch: "reg" = register-resident kernel, default blocked
+    if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
+    else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
+    else e = podp::launch_lu_blk(a, s);
     if (e == cudaSuccess) {
       ++nl;
     } else if (e == cudaErrorNotSupported) {
       cudaGetLastError();
-      e = podp::launch_solve(a, s, &nl);
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const size_t gs = podp::solve_scratch_bytes(c->L.R, sms);
+      double2 *gscr = nullptr;
+      if (gs) e = cudaMallocFromPoolAsync((void **)&gscr, gs, c->pool, s);
+      else e = cudaSuccess;
+      if (e == cudaSuccess) e = podp::launch_solve(a, s, &nl, gscr);
+      if (gscr) cudaFreeAsync(gscr, s);
     }
   }
   if (e == cudaSuccess) {
     ProfScope ps("mpt", s);
-    e = podp::launch_mpt(a, s, &nl);
+    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_mpt_tile(a, s);
+    if (e == cudaSuccess) {
+      ++nl;
+    } else if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = podp::launch_mpt(a, s, &nl);
+    }
   }
   cudaFreeAsync(a.Pws, s);
   g_last_launches = nl;
@@ -391,12 +407,9 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
     for (int q = 1; q < 3; ++q) {
       const long long *tr = trace_buf + q * 1024;
       if (!tr[0]) continue;
-      fprintf(stderr, "omega %d: LU end %lld, end %lld\n", q, tr[700] - tr[0], tr[708] - tr[0]);
-      for (int k = 0; k < 48; k += (k < 8 ? 1 : 8))
-        fprintf(stderr, "  step %2d: start %6lld %6lld %6lld %6lld | pass %6lld %6lld %6lld %6lld | srch %6lld redux %6lld shfl %6lld rcp %6lld end %6lld\n", k,
-                tr[k * 4 + 0] - tr[0], tr[k * 4 + 1] - tr[0], tr[k * 4 + 2] - tr[0], tr[k * 4 + 3] - tr[0],
-                tr[256 + k * 4 + 0] - tr[0], tr[256 + k * 4 + 1] - tr[0], tr[256 + k * 4 + 2] - tr[0], tr[256 + k * 4 + 3] - tr[0],
-                tr[512 + k] - tr[0], tr[640 + k + 1] - tr[0], tr[768 + k + 1] - tr[0], tr[832 + k + 1] - tr[0], tr[576 + k] - tr[0]);
+      fprintf(stderr, "omega %d: assembled %lld, LU done %lld, back-sub done %lld\n", q, tr[1] - tr[0], tr[2] - tr[0], tr[3] - tr[0]);
+      for (int k = 0; k < 16 && tr[16 + 4 * k]; ++k)
+        fprintf(stderr, "  panel %d: start %lld  swaps/U12 %lld  trailing %lld\n", k, tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0]);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");

@@ -42,8 +42,12 @@ struct EvalArgs {
 // Undocumented flag bit (testing only): force the generic shared-memory kernels.
 #define PODP_INTERNAL_FORCE_GENERIC (1 << 16)
 
-cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
-cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch);
+cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
+cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
+cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
+cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch);
+// bytes of global scratch launch_solve needs for this R (0 if the shared-memory variant fits)
+size_t solve_scratch_bytes(int R, int sms);
 cudaError_t launch_mpt(const EvalArgs &a, cudaStream_t s, int *nlaunch);
 cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, const double *snap_d, int n_snap,
                           int n_star, double theta, unsigned long long *lam_bits, unsigned long long *arg_idx,

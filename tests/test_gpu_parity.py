@@ -85,6 +85,17 @@ def test_ragged_and_max_r(torch_cuda, r):
     check_parity(ops, omega, res)
 
 
+@pytest.mark.parametrize("r", [8, 24, 48, 96])
+def test_generic_kernels_parity(torch_cuda, r):
+    """The generic (fallback) kernels stay parity-green: forced with the internal test flag bit 16."""
+    from paper_2307_05590_b200 import FLAG_OUT_R
+    ops = g.make_config0()[0] if r == 8 else g.make_operators(r)
+    omega = g.omega_grid(45)
+    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | (1 << 16))
+    assert (res["info"] == 0).all()
+    check_parity(ops, omega, res)
+
+
 def test_default_flag_outputs_Rt(torch_cuda):
     ops = g.make_operators(24)
     ops.N0 = np.array([[1.0, 0.1, 0.0], [0.1, 2.0, 0.3], [0.0, 0.3, 3.0]])

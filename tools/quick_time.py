@@ -12,14 +12,15 @@ def main():
         ev = Evaluator(c["ops"])
         w = torch.tensor(c["omega"], device="cuda")
         out = ev.alloc_outputs(len(c["omega"]))
+        flags = int(os.environ.get("QT_FLAGS", "0"))
         for _ in range(3):
-            ev.eval(w, out=out)
+            ev.eval(w, out=out, flags=flags)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = 5
         e0.record()
         for _ in range(n):
-            ev.eval(w, out=out)
+            ev.eval(w, out=out, flags=flags)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / n
         nf = len(c["omega"]) * len(c["ops"])
