@@ -1,16 +1,19 @@
-// K2 blocked path: one warp per frequency, panel-blocked right-looking LU with partial pivoting + 3-RHS solve
-// (rows a2-a3).   A(omega) = K + i omega nu M,  B(omega) = b0 + omega b1,  P = A^{-1} B   (eqn:ReducedA)
+// K2 blocked path: panel-blocked right-looking LU with partial pivoting + 3-RHS solve (rows a2-a3).
+//   A(omega) = K + i omega nu M,  B(omega) = b0 + omega b1,  P = A^{-1} B            (eqn:ReducedA)
 //
-// Layout / algorithm (per warp, no inter-warp synchronisation at all):
-//   * [A | B] (R x (R+3) complex, zero-padded to R x NCP) lives in the warp's slice of shared memory.
-//   * For each panel of NB = 8 columns: the panel rows kb..R-1 are held in registers (lane = row, MS slots) and
-//     factored with partial pivoting (redux.sync argmax of an integer magnitude key, lowest row on ties; row swap
-//     by shuffles; pivot reciprocal by MUFU.RCP64H + 2 Newton steps); the 8 row interchanges are then applied to
-//     the columns right of the panel, U12 = L11^{-1} A12 is formed column-wise, and the trailing block
-//     A22 -= L21 U12 runs on the FP64 tensor path (mma.sync.m8n8k4.f64 -> DMMA.8x8x4; a complex 8x8x4 product
-//     is 4 real DMMAs) over 8x8 complex tiles whose C fragments are read/written in shared memory.
-//   * The 3 right-hand sides ride along as columns R..R+2 (forward elimination); back substitution runs from the
-//     U rows in shared memory with the solution column in registers.
+// Layout / algorithm.  A group of W warps owns one frequency at a time; [A | B] (R x (R+3) complex, zero-padded
+// to R x NCP) lives in the group's slice of shared memory.  Columns are cut into 8-wide tile-columns; tile-column
+// c is owned by warp c mod W, which alone applies the row interchanges, forms U12 = L11^{-1} A12 and runs the
+// trailing update A22 -= L21 U12 for it -- so warps never wait on each other except for the panel hand-off.
+//   * Panel b (tile-column b, rows 8b..R-1) is factored in registers by its owner (lane = row, MS slots) with
+//     partial pivoting: redux.sync argmax of an integer magnitude key (lowest row on ties), row interchange and
+//     pivot-row broadcast through a 2-row shared scratch, pivot reciprocal by MUFU.RCP64H + 2 Newton steps.
+//   * Lookahead: the owner of tile-column b+1 first updates that tile-column with panel b, factors panel b+1 and
+//     publishes it (`bar.arrive`, never waits), then updates its other tile-columns; the other warps `bar.sync`.
+//   * The trailing update runs on the FP64 tensor path: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); a complex 8x8x4
+//     product is 4 real DMMAs; C fragments are read/written in shared memory, two tiles interleaved.
+//   * B rides along as columns R..R+2 (forward elimination); back substitution runs from the U rows in shared
+//     memory (one warp per right-hand side, solution column in registers).
 #include <cstdlib>
 
 #include "podp_common.cuh"
@@ -21,53 +24,230 @@ namespace lublk {
 
 constexpr int NB = 8;
 
-template <int R>
+template <int R, int W>
 struct Cfg {
   static_assert(R % 8 == 0, "R must be a multiple of 8 (exact padding)");
   static constexpr int NCP = R + 8;             // columns incl. RHS block (R..R+2) padded to a tile
-  static constexpr int LDA = NCP + 4;           // row stride (complex): LDA = 4 mod 8 for conflict-light tiles
+  static constexpr int NTC = NCP / 8;           // tile-columns
+  static constexpr int LDA = NCP + 4;           // row stride (complex)
   static constexpr int MS = (R + 31) / 32;      // panel row slots per lane
   static constexpr int A_ELEMS = R * LDA;
-  static constexpr int W_BYTES = A_ELEMS * 16 + R * 16 + 2 * 8 * 16 + R * 4 + 16;  // A, 1/U_kk, 2 scratch rows, pivots
-  static constexpr int WARPS = (200 * 1024) / W_BYTES > 16 ? 16 : (200 * 1024) / W_BYTES;
-  static constexpr size_t BYTES = (size_t)WARPS * W_BYTES;
+  static constexpr int G_BYTES = A_ELEMS * 16 + R * 16 + 2 * NB * 16 + R * 4 + 16;  // A, 1/U_kk, scratch, pivots
+  static constexpr int GROUPS_SMEM = (225 * 1024) / G_BYTES;
+  // <= 16 warps per CTA; with W > 1 each group uses 3 named barriers (ids 1..15 available)
+  static constexpr int GROUPS_T = W == 1 ? 16 : ((16 / W) < 5 ? (16 / W) : 5);
+  static constexpr int GROUPS = GROUPS_SMEM < GROUPS_T ? GROUPS_SMEM : GROUPS_T;
+  static constexpr int THREADS = GROUPS * W * 32;
+  static constexpr size_t BYTES = (size_t)GROUPS * G_BYTES;
+  static_assert(GROUPS >= 1, "matrix does not fit in shared memory");
 };
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 #ifndef PODP_LU_TRACE
 #define PODP_LU_TRACE 0
 #endif
+
 }  // namespace lublk
-// dev instrumentation: clock64 stamps of block 0 / warp 0 for its first 4 frequencies (compiled out by default)
+
+// dev instrumentation: clock64 stamps of block 0 / group 0 for its first 4 frequencies (off by default)
 #define LB_TR(slot)                                                                                \
   do {                                                                                             \
     if constexpr (PODP_LU_TRACE)                                                                   \
-      if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && it_ < 4)                        \
+      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && it_ < 4)                         \
         a.trace[it_ * 1024 + (slot)] = clock64();                                                 \
   } while (0)
 
-template <int R>
-__global__ void __launch_bounds__(lublk::Cfg<R>::WARPS * 32, 1) lu_blk_kernel(EvalArgs a) {
-  using C = lublk::Cfg<R>;
-  constexpr int NCP = C::NCP, LDA = C::LDA, MS = C::MS, NB = lublk::NB, NCOL = R + 3;
+template <int R, int W>
+__global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(EvalArgs a) {
+  using C = lublk::Cfg<R, W>;
+  constexpr int NCP = C::NCP, NTC = C::NTC, LDA = C::LDA, MS = C::MS, NB = lublk::NB, NT = W * 32;
+  constexpr int NPAN = R / NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char *wbase = smem_raw + (size_t)warp * C::W_BYTES;
-  double2 *A = reinterpret_cast<double2 *>(wbase);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = wid / W, w = wid % W;
+  unsigned char *gbase = smem_raw + (size_t)grp * C::G_BYTES;
+  double2 *A = reinterpret_cast<double2 *>(gbase);
   double2 *sRinv = A + C::A_ELEMS;
-  double2 *sRowK = sRinv + R, *sRowP = sRowK + NB;  // panel row scratch (old row k, pivot row)
-  int *sPiv = reinterpret_cast<int *>(sRowP + NB);
+  double2 *sRowK = sRinv + R, *sRowP = sRowK + NB;  // panel scratch rows (old row k, pivot row)
+  int *sPiv = reinterpret_cast<int *>(sRowP + NB);  // [R] pivots, [R] group status
+  const int bar0 = 1 + 3 * grp;  // ids bar0, bar0+1 (alternating panel hand-offs), bar0+2 (full group)
   const int64_t total = (int64_t)a.n_obj * a.F;
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
   const unsigned FULL = 0xffffffffu;
-
+  const int ngroups_total = gridDim.x * C::GROUPS;
   int it_ = -1;
-  for (int64_t t = (int64_t)blockIdx.x * C::WARPS + warp; t < total; t += (int64_t)gridDim.x * C::WARPS) {
+  (void)it_;
+  (void)NCP;
+
+  // ---- panel factorisation of tile-column b by the calling warp (sets info != 0 on a zero pivot) -------------
+  auto factor_panel = [&](int b, int &info) __attribute__((always_inline)) {
+    const int kb = b * NB;
+    double2 pn[MS][NB];
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const int i = kb + lane + 32 * m;
+#pragma unroll
+      for (int c = 0; c < NB; ++c) pn[m][c] = (i < R) ? A[i * LDA + kb + c] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const int kr = kb + j;  // pivot position: lane j, slot 0
+      unsigned key = 0u;
+#pragma unroll
+      for (int m = 0; m < MS; ++m) {
+        const int i = kb + lane + 32 * m;
+        const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - i);
+        if (i >= kr && i < R && kk > key) key = kk;
+      }
+      const unsigned best = __reduce_max_sync(FULL, key);
+      if ((best >> 7) == 0u) {
+        if (info == 0) info = kr + 1;
+        return;
+      }
+      const int p = 127 - (int)(best & 127u);
+      const int lp = (p - kb) & 31, mp = (p - kb) >> 5;
+      // stage pivot row p and row kr in shared memory
+      if (lane == lp) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m)
+          if (m == mp) {
+#pragma unroll
+            for (int c = 0; c < NB; ++c) sRowP[c] = pn[m][c];
+          }
+      }
+      if (lane == j && p != kr) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) sRowK[c] = pn[0][c];
+      }
+      if (lane == 0) sPiv[kr] = p;
+      __syncwarp();
+      const double2 pv = sRowP[j];
+      double2 u[NB];
+#pragma unroll
+      for (int c = j + 1; c < NB; ++c) u[c] = sRowP[c];
+      if (p != kr) {
+        if (lane == lp) {
+#pragma unroll
+          for (int m = 0; m < MS; ++m)
+            if (m == mp) {
+#pragma unroll
+              for (int c = 0; c < NB; ++c) pn[m][c] = sRowK[c];
+            }
+        }
+        if (lane == j) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c) pn[0][c] = sRowP[c];
+        }
+      }
+      const double2 rc = crecip_fast(pv);
+      if (lane == 0) sRinv[kr] = rc;
+      double2 l[MS];
+#pragma unroll
+      for (int m = 0; m < MS; ++m) {
+        const int i = kb + lane + 32 * m;
+        const bool act = i > kr && i < R;
+        l[m] = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
+        if (act) pn[m][j] = l[m];
+      }
+#pragma unroll
+      for (int c = j + 1; c < NB; ++c) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m) pn[m][c] = cfms(l[m], u[c], pn[m][c]);
+      }
+      __syncwarp();  // scratch rows are reused by the next column
+    }
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const int i = kb + lane + 32 * m;
+      if (i < R) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) A[i * LDA + kb + c] = pn[m][c];
+      }
+    }
+  };
+
+  // ---- apply panel b (interchanges, U12, trailing update) to tile-column tcol (owned by the calling warp) -------
+  auto update_tile_col = [&](int b, int tcol) __attribute__((always_inline)) {
+    const int kb = b * NB;
+    const int col0 = tcol * 8;
+    // (1) interchanges + U12 = L11^{-1} A12: lanes 0..7 own one column each
+    if (lane < 8) {
+      const int col = col0 + lane;
+      double2 x[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int p = sPiv[kb + j];
+        const double2 vk = A[(kb + j) * LDA + col];
+        if (p != kb + j) {
+          x[j] = A[p * LDA + col];
+          A[p * LDA + col] = vk;
+        } else {
+          x[j] = vk;
+        }
+      }
+#pragma unroll
+      for (int j = 1; j < NB; ++j) {
+#pragma unroll
+        for (int tt = 0; tt < j; ++tt) x[j] = cfms(A[(kb + j) * LDA + kb + tt], x[tt], x[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) A[(kb + j) * LDA + col] = x[j];
+    }
+    __syncwarp();
+    // (2) A22[:, tile] -= L21 U12[:, tile] on 8x8 complex tiles; two row-tiles interleaved
+    const int arow = lane >> 2, acol = lane & 3;
+    const int bk = lane & 3, bcol = lane >> 2;
+    const int crow = lane >> 2, ccol = 2 * (lane & 3);
+    const double2 b0 = A[(kb + bk) * LDA + col0 + bcol], b1 = A[(kb + 4 + bk) * LDA + col0 + bcol];
+    auto tile = [&](double &cr0, double &cr1, double &ci0, double &ci1, double2 a0, double2 a1)
+        __attribute__((always_inline)) {
+      // C -= A B (complex): C_re += (-A_re) B_re + A_im B_im ; C_im += (-A_re) B_im + (-A_im) B_re
+      lublk::dmma(cr0, cr1, -a0.x, b0.x);
+      lublk::dmma(ci0, ci1, -a0.x, b0.y);
+      lublk::dmma(cr0, cr1, a0.y, b0.y);
+      lublk::dmma(ci0, ci1, -a0.y, b0.x);
+      lublk::dmma(cr0, cr1, -a1.x, b1.x);
+      lublk::dmma(ci0, ci1, -a1.x, b1.y);
+      lublk::dmma(cr0, cr1, a1.y, b1.y);
+      lublk::dmma(ci0, ci1, -a1.y, b1.x);
+    };
+    int tr = kb + NB;
+    for (; tr + 8 < R; tr += 16) {
+      const double2 a0 = A[(tr + arow) * LDA + kb + acol], a1 = A[(tr + arow) * LDA + kb + 4 + acol];
+      const double2 e0 = A[(tr + 8 + arow) * LDA + kb + acol], e1 = A[(tr + 8 + arow) * LDA + kb + 4 + acol];
+      double2 *cp = A + (tr + crow) * LDA + col0 + ccol;
+      double2 *dp = cp + 8 * LDA;
+      const double2 c0 = cp[0], c1 = cp[1], d0 = dp[0], d1 = dp[1];
+      double cr0 = c0.x, cr1 = c1.x, ci0 = c0.y, ci1 = c1.y;
+      double dr0 = d0.x, dr1 = d1.x, di0 = d0.y, di1 = d1.y;
+      tile(cr0, cr1, ci0, ci1, a0, a1);
+      tile(dr0, dr1, di0, di1, e0, e1);
+      cp[0] = make_double2(cr0, ci0);
+      cp[1] = make_double2(cr1, ci1);
+      dp[0] = make_double2(dr0, di0);
+      dp[1] = make_double2(dr1, di1);
+    }
+    if (tr < R) {
+      const double2 a0 = A[(tr + arow) * LDA + kb + acol], a1 = A[(tr + arow) * LDA + kb + 4 + acol];
+      double2 *cp = A + (tr + crow) * LDA + col0 + ccol;
+      const double2 c0 = cp[0], c1 = cp[1];
+      double cr0 = c0.x, cr1 = c1.x, ci0 = c0.y, ci1 = c1.y;
+      tile(cr0, cr1, ci0, ci1, a0, a1);
+      cp[0] = make_double2(cr0, ci0);
+      cp[1] = make_double2(cr1, ci1);
+    }
+    __syncwarp();
+  };
+
+  for (int64_t t = (int64_t)blockIdx.x * C::GROUPS + grp; t < total; t += ngroups_total) {
     ++it_;
     const int obj = (int)(t / a.F);
     const int64_t f = t - (int64_t)obj * a.F;
@@ -75,28 +255,28 @@ __global__ void __launch_bounds__(lublk::Cfg<R>::WARPS * 32, 1) lu_blk_kernel(Ev
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
     LB_TR(0);
-    // ---- a2: assemble [A | B | 0] ----------------------------------------------------------------------------
+    // ---- a2: assemble [A | B | 0] (all W warps; K, M streamed from L2 with 12 loads in flight per lane) ----------
     {
       const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
       const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
-      static_assert((R * R) % 32 == 0, "R*R must be a multiple of 32");
-      constexpr int PER = (R * R) / 32;
+      constexpr int PER = (R * R + NT - 1) / NT;
       constexpr int BATCH = 12;
+      const int gl = w * 32 + lane;
 #pragma unroll 1
       for (int e0 = 0; e0 < PER; e0 += BATCH) {
         double2 kk[BATCH], mm[BATCH];
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
-          const int e = (e0 + q) * 32 + lane;
-          if (e0 + q < PER) {
+          const int e = (e0 + q) * NT + gl;
+          if (e0 + q < PER && e < R * R) {
             kk[q] = __ldg(gK + e);
             mm[q] = __ldg(gM + e);
           }
         }
 #pragma unroll
         for (int q = 0; q < BATCH; ++q) {
-          const int e = (e0 + q) * 32 + lane;
-          if (e0 + q < PER) {
+          const int e = (e0 + q) * NT + gl;
+          if (e0 + q < PER && e < R * R) {
             const int i = e / R, j = e - i * R;
             A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk[q].x), fma(s, mm[q].x, kk[q].y));
           }
@@ -104,7 +284,7 @@ __global__ void __launch_bounds__(lublk::Cfg<R>::WARPS * 32, 1) lu_blk_kernel(Ev
       }
       const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
       const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
-      for (int e = lane; e < 8 * R; e += 32) {
+      for (int e = gl; e < 8 * R; e += NT) {
         const int i = e >> 3, c = e & 7;
         double2 v = make_double2(0.0, 0.0);
         if (c < 3) {
@@ -114,273 +294,156 @@ __global__ void __launch_bounds__(lublk::Cfg<R>::WARPS * 32, 1) lu_blk_kernel(Ev
         A[i * LDA + R + c] = v;
       }
     }
-    __syncwarp();
+    if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
     LB_TR(1);
     int info = isfinite(om) ? 0 : -1;
-
-    // ---- a3: blocked LU with partial pivoting --------------------------------------------------------------------
-    for (int kb = 0; kb < R && info == 0; kb += NB) {
-      LB_TR(16 + (kb / NB) * 4);
-      // (1) panel factorisation in registers: lane owns rows kb + lane + 32 m
-      double2 pn[MS][NB];
-#pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        const int i = kb + lane + 32 * m;
-#pragma unroll
-        for (int c = 0; c < NB; ++c) pn[m][c] = (i < R) ? A[i * LDA + kb + c] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int kr = kb + j;  // pivot row position (held by lane j, slot 0)
-        unsigned key = 0u;
-#pragma unroll
-        for (int m = 0; m < MS; ++m) {
-          const int i = kb + lane + 32 * m;
-          const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - i);
-          if (i >= kr && i < R && kk > key) key = kk;
-        }
-        const unsigned best = __reduce_max_sync(FULL, key);
-        if ((best >> 7) == 0u) {  // exactly zero pivot column
-          info = kr + 1;
-          break;
-        }
-        const int p = 127 - (int)(best & 127u);
-        const int lp = (p - kb) & 31, mp = (p - kb) >> 5;
-        if (lane == 0) sPiv[kr] = p;
-        // stage row kr (lane j, slot 0) and the pivot row p (lane lp, slot mp) in shared memory
-        if (lane == j) {
-#pragma unroll
-          for (int c = 0; c < NB; ++c) sRowK[c] = pn[0][c];
-        }
-        if (lane == lp) {
-#pragma unroll
-          for (int m = 0; m < MS; ++m)
-            if (m == mp) {
-#pragma unroll
-              for (int c = 0; c < NB; ++c) sRowP[c] = pn[m][c];
-            }
-        }
-        __syncwarp();
-        if (p != kr) {
-          if (lane == lp) {
-#pragma unroll
-            for (int m = 0; m < MS; ++m)
-              if (m == mp) {
-#pragma unroll
-                for (int c = 0; c < NB; ++c) pn[m][c] = sRowK[c];
-              }
-          }
-          if (lane == j) {
-#pragma unroll
-            for (int c = 0; c < NB; ++c) pn[0][c] = sRowP[c];
-          }
-        }
-        const double2 pv = sRowP[j];
-        const double2 rc = crecip_fast(pv);
-        if (lane == 0) sRinv[kr] = rc;
-        double2 l[MS];
-#pragma unroll
-        for (int m = 0; m < MS; ++m) {
-          const int i = kb + lane + 32 * m;
-          l[m] = (i > kr && i < R) ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
-          if (i > kr && i < R) pn[m][j] = l[m];
-        }
-#pragma unroll
-        for (int c = j + 1; c < NB; ++c) {
-          const double2 u = sRowP[c];
-#pragma unroll
-          for (int m = 0; m < MS; ++m) pn[m][c] = cfms(l[m], u, pn[m][c]);
-        }
-        __syncwarp();  // scratch rows reused by the next column
-      }
-      if (info != 0) break;
-      // write the factored panel back (L21 multipliers, U11)
-#pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        const int i = kb + lane + 32 * m;
-        if (i < R) {
-#pragma unroll
-          for (int c = 0; c < NB; ++c) A[i * LDA + kb + c] = pn[m][c];
-        }
-      }
+    // ---- a3: blocked LU -- panel 0 by its owner (warp 0); group status lives in sPiv[R] ---------------------------
+    if (w == 0) {
+      if (info == 0) factor_panel(0, info);
+      if (lane == 0) sPiv[R] = info;
       __syncwarp();
-      LB_TR(17 + (kb / NB) * 4);
-      // (2) row interchanges + U12 = L11^{-1} A12 for the columns right of the panel (lane = column)
-      for (int col = kb + NB + lane; col < NCP; col += 32) {
-        double2 x[NB];
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int p = sPiv[kb + j];
-          const double2 vk = A[(kb + j) * LDA + col];
-          if (p != kb + j) {
-            const double2 vp = A[p * LDA + col];
-            A[p * LDA + col] = vk;
-            x[j] = vp;
-          } else {
-            x[j] = vk;
-          }
-          // rows kb+j' (j' > j) not yet swapped may be read later: keep swapped values in registers only
-          A[(kb + j) * LDA + col] = x[j];
-        }
-#pragma unroll
-        for (int j = 1; j < NB; ++j) {
-#pragma unroll
-          for (int tt = 0; tt < j; ++tt) x[j] = cfms(A[(kb + j) * LDA + kb + tt], x[tt], x[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < NB; ++j) A[(kb + j) * LDA + col] = x[j];
-      }
-      __syncwarp();
-      LB_TR(18 + (kb / NB) * 4);
-      // (3) trailing update A22 -= L21 U12 on 8x8 complex tiles (DMMA)
-      const int r0 = kb + NB;
-      const int arow = lane >> 2, acol = lane & 3;   // A fragment (8x4): row, k
-      const int bk = lane & 3, bcol = lane >> 2;      // B fragment (4x8): k, col
-      const int crow = lane >> 2, ccol = 2 * (lane & 3);
-      for (int tr = r0; tr < R; tr += 8) {
-        // A fragments (L21 rows tr..tr+7, k = kb..kb+7): two k-steps of 4
-        const double2 a0 = A[(tr + arow) * LDA + kb + acol];
-        const double2 a1 = A[(tr + arow) * LDA + kb + 4 + acol];
-        auto tile = [&](double &cr0, double &cr1, double &ci0, double &ci1, double2 b0, double2 b1)
-            __attribute__((always_inline)) {
-          // C -= A B  (complex): C_re += (-A_re) B_re + A_im B_im ; C_im += (-A_re) B_im + (-A_im) B_re
-          lublk::dmma(cr0, cr1, -a0.x, b0.x);
-          lublk::dmma(ci0, ci1, -a0.x, b0.y);
-          lublk::dmma(cr0, cr1, a0.y, b0.y);
-          lublk::dmma(ci0, ci1, -a0.y, b0.x);
-          lublk::dmma(cr0, cr1, -a1.x, b1.x);
-          lublk::dmma(ci0, ci1, -a1.x, b1.y);
-          lublk::dmma(cr0, cr1, a1.y, b1.y);
-          lublk::dmma(ci0, ci1, -a1.y, b1.x);
-        };
-        int tc = r0;
-        for (; tc + 8 < NCP; tc += 16) {
-          const double2 b0 = A[(kb + bk) * LDA + tc + bcol], b1 = A[(kb + 4 + bk) * LDA + tc + bcol];
-          const double2 e0 = A[(kb + bk) * LDA + tc + 8 + bcol], e1 = A[(kb + 4 + bk) * LDA + tc + 8 + bcol];
-          double2 *cp = A + (tr + crow) * LDA + tc + ccol;
-          const double2 c0 = cp[0], c1 = cp[1], d0 = cp[8], d1 = cp[9];
-          double cr0 = c0.x, cr1 = c1.x, ci0 = c0.y, ci1 = c1.y;
-          double dr0 = d0.x, dr1 = d1.x, di0 = d0.y, di1 = d1.y;
-          tile(cr0, cr1, ci0, ci1, b0, b1);
-          tile(dr0, dr1, di0, di1, e0, e1);
-          cp[0] = make_double2(cr0, ci0);
-          cp[1] = make_double2(cr1, ci1);
-          cp[8] = make_double2(dr0, di0);
-          cp[9] = make_double2(dr1, di1);
-        }
-        if (tc < NCP) {
-          const double2 b0 = A[(kb + bk) * LDA + tc + bcol], b1 = A[(kb + 4 + bk) * LDA + tc + bcol];
-          double2 *cp = A + (tr + crow) * LDA + tc + ccol;
-          const double2 c0 = cp[0], c1 = cp[1];
-          double cr0 = c0.x, cr1 = c1.x, ci0 = c0.y, ci1 = c1.y;
-          tile(cr0, cr1, ci0, ci1, b0, b1);
-          cp[0] = make_double2(cr0, ci0);
-          cp[1] = make_double2(cr1, ci1);
-        }
-      }
-      __syncwarp();
+      if constexpr (W > 1) lublk::bar_arrive(bar0, NT);
     }
-
+    for (int b = 0; b < NPAN; ++b) {
+      const int owner = b % W;
+      if constexpr (W > 1) {
+        if (w != owner) lublk::bar_sync(bar0 + (b & 1), NT);
+      } else {
+        __syncwarp();
+      }
+      info = sPiv[R];
+      const bool next = b + 1 < NPAN;
+      const int nowner = (b + 1) % W;
+      if (info == 0 && next && w == nowner) {
+        // lookahead: the owner of tile-column b+1 updates it, factors panel b+1 and publishes it
+        update_tile_col(b, b + 1);
+        int inf2 = 0;
+        factor_panel(b + 1, inf2);
+        if (lane == 0) sPiv[R] = inf2;
+        __syncwarp();
+      }
+      if (next && w == nowner) {
+        if constexpr (W > 1) lublk::bar_arrive(bar0 + ((b + 1) & 1), NT);
+      }
+      if (info == 0) {
+        for (int tc = b + 1; tc < NTC; ++tc) {
+          if (tc % W != w) continue;
+          if (next && tc == b + 1) continue;  // done in the lookahead
+          update_tile_col(b, tc);
+        }
+      }
+    }
+    if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
+    info = sPiv[R];
     LB_TR(2);
-    // ---- back substitution U x = y (lane = row), 3 right-hand sides ------------------------------------------------
+    // ---- back substitution U x = y (warp c handles right-hand side c; lane = row) --------------------------------
     double2 *Pw = a.Pws + (size_t)t * 3 * R;
-    if (info == 0) {
-      double2 y[MS][3];
+    for (int c = w; c < 3; c += W) {
+      if (info == 0) {
+        double2 y[MS];
 #pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        const int i = lane + 32 * m;
+        for (int m = 0; m < MS; ++m) {
+          const int i = lane + 32 * m;
+          y[m] = (i < R) ? A[i * LDA + R + c] : make_double2(0.0, 0.0);
+        }
+        double2 ukn[MS];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) y[m][c] = (i < R) ? A[i * LDA + R + c] : make_double2(0.0, 0.0);
-      }
-      double2 ukn[MS];
+        for (int m = 0; m < MS; ++m) {
+          const int i = lane + 32 * m;
+          ukn[m] = (i < R - 1) ? A[i * LDA + R - 1] : make_double2(0.0, 0.0);
+        }
+        double2 rkn = sRinv[R - 1];
 #pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        const int i = lane + 32 * m;
-        ukn[m] = (i < R - 1) ? A[i * LDA + R - 1] : make_double2(0.0, 0.0);
-      }
-      double2 rkn = sRinv[R - 1];
-#pragma unroll
-      for (int mb = MS - 1; mb >= 0; --mb) {
-        const int khi = (32 * mb + 31 < R - 1) ? 32 * mb + 31 : R - 1;
+        for (int mb = MS - 1; mb >= 0; --mb) {
+          const int khi = (32 * mb + 31 < R - 1) ? 32 * mb + 31 : R - 1;
 #pragma unroll 2
-        for (int k = khi; k >= 32 * mb; --k) {
-          const double2 rk = rkn;
-          double2 uk[MS];
+          for (int k = khi; k >= 32 * mb; --k) {
+            const double2 rk = rkn;
+            double2 uk[MS];
 #pragma unroll
-          for (int m = 0; m < MS; ++m) uk[m] = ukn[m];
-          if (k > 0) {
+            for (int m = 0; m < MS; ++m) uk[m] = ukn[m];
+            if (k > 0) {
 #pragma unroll
-            for (int m = 0; m < MS; ++m) {
-              const int i = lane + 32 * m;
-              ukn[m] = (i < k - 1) ? A[i * LDA + k - 1] : make_double2(0.0, 0.0);
+              for (int m = 0; m < MS; ++m) {
+                const int i = lane + 32 * m;
+                ukn[m] = (i < k - 1) ? A[i * LDA + k - 1] : make_double2(0.0, 0.0);
+              }
+              rkn = sRinv[k - 1];
             }
-            rkn = sRinv[k - 1];
-          }
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
             double2 yk;
-            yk.x = __shfl_sync(FULL, y[mb][c].x, k & 31);
-            yk.y = __shfl_sync(FULL, y[mb][c].y, k & 31);
+            yk.x = __shfl_sync(FULL, y[mb].x, k & 31);
+            yk.y = __shfl_sync(FULL, y[mb].y, k & 31);
             const double2 xk = cmul(yk, rk);
 #pragma unroll
             for (int m = 0; m <= mb; ++m) {
               const int i = lane + 32 * m;
-              if (i < k) y[m][c] = cfms(uk[m], xk, y[m][c]);
-              else if (i == k) y[m][c] = xk;
+              if (i < k) y[m] = cfms(uk[m], xk, y[m]);
+              else if (i == k) y[m] = xk;
             }
           }
         }
-      }
 #pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        const int i = lane + 32 * m;
-        if (i < R) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            Pw[c * R + i] = y[m][c];
-            if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = y[m][c];
+        for (int m = 0; m < MS; ++m) {
+          const int i = lane + 32 * m;
+          if (i < R) {
+            Pw[c * R + i] = y[m];
+            if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = y[m];
           }
         }
+      } else {
+        for (int i = lane; i < R; i += 32) Pw[c * R + i] = make_double2(nanv, nanv);
+        if (a.P_out)
+          for (int i = lane; i < a.r; i += 32)
+            reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = make_double2(nanv, nanv);
       }
-    } else {
-      for (int e = lane; e < 3 * R; e += 32) Pw[e] = make_double2(nanv, nanv);
-      if (a.P_out)
-        for (int e = lane; e < 3 * a.r; e += 32)
-          reinterpret_cast<double2 *>(a.P_out)[(size_t)t * 3 * a.r + e] = make_double2(nanv, nanv);
     }
     LB_TR(3);
-    if (a.info && lane == 0) a.info[t] = info;
-    __syncwarp();
+    if (a.info && w == 0 && lane == 0) a.info[t] = info;
+    if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
   }
 }
 
-template <int R>
+template <int R, int W>
 static cudaError_t launch_lu_blk_t(const EvalArgs &a, cudaStream_t s) {
-  using C = lublk::Cfg<R>;
-  auto kern = lu_blk_kernel<R>;
+  using C = lublk::Cfg<R, W>;
+  auto kern = lu_blk_kernel<R, W>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t total = (int64_t)a.n_obj * a.F;
-  int64_t blocks = (total + C::WARPS - 1) / C::WARPS;
+  int64_t blocks = (total + C::GROUPS - 1) / C::GROUPS;
   if (blocks > sms) blocks = sms;
-  kern<<<(unsigned)blocks, C::WARPS * 32, C::BYTES, s>>>(a);
+  kern<<<(unsigned)blocks, C::THREADS, C::BYTES, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
+  const char *v = getenv("PODP_LU_W");
+  // measured on B200 (tools/quick_time.py): one warp per frequency is best for r <= 32, two for r = 40..56,
+  // four for r >= 64 (shared memory then holds a single frequency per SM)
+  const int wv = v ? atoi(v) : (a.L.R >= 64 ? 4 : (a.L.R >= 40 ? 2 : 1));
   switch (a.L.R) {
-    case 8: return launch_lu_blk_t<8>(a, s);
-    case 16: return launch_lu_blk_t<16>(a, s);
-    case 24: return launch_lu_blk_t<24>(a, s);
-    case 32: return launch_lu_blk_t<32>(a, s);
-    case 40: return launch_lu_blk_t<40>(a, s);
-    case 48: return launch_lu_blk_t<48>(a, s);
-    case 56: return launch_lu_blk_t<56>(a, s);
-    case 64: return launch_lu_blk_t<64>(a, s);
+#define PODP_CASE(RR)                                 \
+  case RR:                                            \
+    if (wv == 1) return launch_lu_blk_t<RR, 1>(a, s); \
+    if (wv == 2) return launch_lu_blk_t<RR, 2>(a, s); \
+    return launch_lu_blk_t<RR, 4>(a, s);
+    PODP_CASE(8)
+    PODP_CASE(16)
+    PODP_CASE(24)
+    PODP_CASE(32)
+    PODP_CASE(40)
+    PODP_CASE(48)
+    PODP_CASE(56)
+    PODP_CASE(64)
+    PODP_CASE(72)
+    PODP_CASE(80)
+    PODP_CASE(88)
+    PODP_CASE(96)
+#undef PODP_CASE
     default: return cudaErrorNotSupported;
   }
 }

@@ -375,6 +375,7 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
     const char *lv = getenv("PODP_LU_IMPL");  // dev switch: "reg" = register-resident kernel, default blocked
     if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
     else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
+    else if (lv && lv[0] == 'p') e = podp::launch_lu_pw(a, s);
     else e = podp::launch_lu_blk(a, s);
     if (e == cudaSuccess) {
       ++nl;

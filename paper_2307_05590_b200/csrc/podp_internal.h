@@ -45,6 +45,7 @@ struct EvalArgs {
 cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
+cudaError_t launch_lu_pw(const EvalArgs &a, cudaStream_t s);     // cudaErrorNotSupported if no instantiation
 cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch);
 // bytes of global scratch launch_solve needs for this R (0 if the shared-memory variant fits)
 size_t solve_scratch_bytes(int R, int sms);
