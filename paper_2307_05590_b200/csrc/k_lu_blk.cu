@@ -29,7 +29,7 @@ struct Cfg {
   static_assert(R % 8 == 0, "R must be a multiple of 8 (exact padding)");
   static constexpr int NCP = R + 8;             // columns incl. RHS block (R..R+2) padded to a tile
   static constexpr int NTC = NCP / 8;           // tile-columns
-  static constexpr int LDA = NCP + 4;           // row stride (complex)
+  static constexpr int LDA = NCP + 1;           // row stride (complex), odd: 16-byte-bank rotation per row
   static constexpr int MS = (R + 31) / 32;      // panel row slots per lane
   static constexpr int A_ELEMS = R * LDA;
   static constexpr int G_BYTES = A_ELEMS * 16 + R * 16 + 2 * NB * 16 + R * 4 + 16;  // A, 1/U_kk, scratch, pivots
@@ -61,7 +61,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.ar
 #define LB_TR(slot)                                                                                \
   do {                                                                                             \
     if constexpr (PODP_LU_TRACE)                                                                   \
-      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && it_ < 4)                         \
+      if (a.trace && blockIdx.x == 0 && grp == 0 && w == 0 && lane == 0 && it_ < 4)              \
         a.trace[it_ * 1024 + (slot)] = clock64();                                                 \
   } while (0)
 
@@ -88,44 +88,44 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
   (void)NCP;
 
   // ---- panel factorisation of tile-column b by the calling warp (sets info != 0 on a zero pivot) -------------
+  // Rows never move inside the panel: lane owns the panel rows loaded from positions kb + lane + 32 m and tracks
+  // each row's current position (LAPACK interchange semantics).  The pivot search key carries the POSITION, so
+  // ties resolve to the lowest position as in izamax; only the pivot row is broadcast (8 values via smem).
   auto factor_panel = [&](int b, int &info) __attribute__((always_inline)) {
     const int kb = b * NB;
     double2 pn[MS][NB];
+    int pos[MS];
 #pragma unroll
     for (int m = 0; m < MS; ++m) {
       const int i = kb + lane + 32 * m;
+      pos[m] = i < R ? i : 1 << 20;
 #pragma unroll
       for (int c = 0; c < NB; ++c) pn[m][c] = (i < R) ? A[i * LDA + kb + c] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      const int kr = kb + j;  // pivot position: lane j, slot 0
+      const int kr = kb + j;
       unsigned key = 0u;
 #pragma unroll
       for (int m = 0; m < MS; ++m) {
-        const int i = kb + lane + 32 * m;
-        const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - i);
-        if (i >= kr && i < R && kk > key) key = kk;
+        const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - pos[m]);
+        if (pos[m] >= kr && pos[m] < R && kk > key) key = kk;
       }
       const unsigned best = __reduce_max_sync(FULL, key);
       if ((best >> 7) == 0u) {
         if (info == 0) info = kr + 1;
         return;
       }
-      const int p = 127 - (int)(best & 127u);
-      const int lp = (p - kb) & 31, mp = (p - kb) >> 5;
-      // stage pivot row p and row kr in shared memory
-      if (lane == lp) {
+      const int p = 127 - (int)(best & 127u);  // pivot position
+      // the row now at position p is the pivot row: broadcast its panel values; positions kr <-> p swap
+      bool mine[MS];
 #pragma unroll
-        for (int m = 0; m < MS; ++m)
-          if (m == mp) {
+      for (int m = 0; m < MS; ++m) {
+        mine[m] = pos[m] == p;
+        if (mine[m]) {
 #pragma unroll
-            for (int c = 0; c < NB; ++c) sRowP[c] = pn[m][c];
-          }
-      }
-      if (lane == j && p != kr) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) sRowK[c] = pn[0][c];
+          for (int c = j; c < NB; ++c) sRowP[c] = pn[m][c];
+        }
       }
       if (lane == 0) sPiv[kr] = p;
       __syncwarp();
@@ -133,43 +133,26 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       double2 u[NB];
 #pragma unroll
       for (int c = j + 1; c < NB; ++c) u[c] = sRowP[c];
-      if (p != kr) {
-        if (lane == lp) {
 #pragma unroll
-          for (int m = 0; m < MS; ++m)
-            if (m == mp) {
-#pragma unroll
-              for (int c = 0; c < NB; ++c) pn[m][c] = sRowK[c];
-            }
-        }
-        if (lane == j) {
-#pragma unroll
-          for (int c = 0; c < NB; ++c) pn[0][c] = sRowP[c];
-        }
-      }
+      for (int m = 0; m < MS; ++m) pos[m] = mine[m] ? kr : (pos[m] == kr ? p : pos[m]);
       const double2 rc = crecip_fast(pv);
       if (lane == 0) sRinv[kr] = rc;
-      double2 l[MS];
 #pragma unroll
       for (int m = 0; m < MS; ++m) {
-        const int i = kb + lane + 32 * m;
-        const bool act = i > kr && i < R;
-        l[m] = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
-        if (act) pn[m][j] = l[m];
-      }
+        const bool act = pos[m] > kr && pos[m] < R;
+        const double2 l = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
+        if (act) pn[m][j] = l;
 #pragma unroll
-      for (int c = j + 1; c < NB; ++c) {
-#pragma unroll
-        for (int m = 0; m < MS; ++m) pn[m][c] = cfms(l[m], u[c], pn[m][c]);
+        for (int c = j + 1; c < NB; ++c) pn[m][c] = cfms(l, u[c], pn[m][c]);
       }
-      __syncwarp();  // scratch rows are reused by the next column
+      __syncwarp();  // scratch row reused by the next column
     }
+    // write the factored panel back at the rows' final positions (L21 multipliers, U11)
 #pragma unroll
     for (int m = 0; m < MS; ++m) {
-      const int i = kb + lane + 32 * m;
-      if (i < R) {
+      if (pos[m] < R) {
 #pragma unroll
-        for (int c = 0; c < NB; ++c) A[i * LDA + kb + c] = pn[m][c];
+        for (int c = 0; c < NB; ++c) A[pos[m] * LDA + kb + c] = pn[m][c];
       }
     }
   };
@@ -311,6 +294,7 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       } else {
         __syncwarp();
       }
+      LB_TR(16 + 4 * b);
       info = sPiv[R];
       const bool next = b + 1 < NPAN;
       const int nowner = (b + 1) % W;
@@ -325,6 +309,7 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       if (next && w == nowner) {
         if constexpr (W > 1) lublk::bar_arrive(bar0 + ((b + 1) & 1), NT);
       }
+      LB_TR(17 + 4 * b);
       if (info == 0) {
         for (int tc = b + 1; tc < NTC; ++tc) {
           if (tc % W != w) continue;
@@ -332,69 +317,70 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
           update_tile_col(b, tc);
         }
       }
+      LB_TR(18 + 4 * b);
     }
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
     info = sPiv[R];
     LB_TR(2);
-    // ---- back substitution U x = y (warp c handles right-hand side c; lane = row) --------------------------------
+    // ---- back substitution U x = y, blocked (warp 0): the NPAN diagonal 8x8 blocks of U are inverted in parallel
+    //      (one lane per block column; the strictly upper part of each inverse is stored transposed in the dead
+    //      L11 slots), then NPAN block steps x_b = Dinv_b y_b, y_above -= U_above,b x_b (lanes over rows x rhs).
     double2 *Pw = a.Pws + (size_t)t * 3 * R;
-    for (int c = w; c < 3; c += W) {
+    if (w == 0) {
       if (info == 0) {
-        double2 y[MS];
+        for (int task = lane; task < NPAN * 8; task += 32) {
+          const int kb = (task >> 3) * 8, c = task & 7;
+          double2 x[8];
 #pragma unroll
-        for (int m = 0; m < MS; ++m) {
-          const int i = lane + 32 * m;
-          y[m] = (i < R) ? A[i * LDA + R + c] : make_double2(0.0, 0.0);
-        }
-        double2 ukn[MS];
+          for (int j = 0; j < 8; ++j) x[j] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int m = 0; m < MS; ++m) {
-          const int i = lane + 32 * m;
-          ukn[m] = (i < R - 1) ? A[i * LDA + R - 1] : make_double2(0.0, 0.0);
-        }
-        double2 rkn = sRinv[R - 1];
+          for (int j = 7; j >= 0; --j) {
+            if (j == c) x[j] = sRinv[kb + j];
+            if (j < c) {
+              double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int mb = MS - 1; mb >= 0; --mb) {
-          const int khi = (32 * mb + 31 < R - 1) ? 32 * mb + 31 : R - 1;
-#pragma unroll 2
-          for (int k = khi; k >= 32 * mb; --k) {
-            const double2 rk = rkn;
-            double2 uk[MS];
-#pragma unroll
-            for (int m = 0; m < MS; ++m) uk[m] = ukn[m];
-            if (k > 0) {
-#pragma unroll
-              for (int m = 0; m < MS; ++m) {
-                const int i = lane + 32 * m;
-                ukn[m] = (i < k - 1) ? A[i * LDA + k - 1] : make_double2(0.0, 0.0);
-              }
-              rkn = sRinv[k - 1];
-            }
-            double2 yk;
-            yk.x = __shfl_sync(FULL, y[mb].x, k & 31);
-            yk.y = __shfl_sync(FULL, y[mb].y, k & 31);
-            const double2 xk = cmul(yk, rk);
-#pragma unroll
-            for (int m = 0; m <= mb; ++m) {
-              const int i = lane + 32 * m;
-              if (i < k) y[m] = cfms(uk[m], xk, y[m]);
-              else if (i == k) y[m] = xk;
+              for (int tt = j + 1; tt < 8; ++tt)
+                if (tt <= c) acc = cfma(A[(kb + j) * LDA + kb + tt], x[tt], acc);
+              x[j] = cmul(make_double2(-acc.x, -acc.y), sRinv[kb + j]);
             }
           }
-        }
 #pragma unroll
-        for (int m = 0; m < MS; ++m) {
-          const int i = lane + 32 * m;
-          if (i < R) {
-            Pw[c * R + i] = y[m];
-            if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = y[m];
+          for (int j = 0; j < 8; ++j)
+            if (j < c) A[(kb + c) * LDA + kb + j] = x[j];  // Dinv[j][c] stored at (c, j)
+        }
+        __syncwarp();
+        for (int b = NPAN - 1; b >= 0; --b) {
+          const int kb = b * 8;
+          double2 xb = make_double2(0.0, 0.0);
+          const int r = lane / 3, c = lane - 3 * (lane / 3);
+          if (lane < 24) {
+            xb = cmul(sRinv[kb + r], A[(kb + r) * LDA + R + c]);
+#pragma unroll
+            for (int tt = 1; tt < 8; ++tt)
+              if (tt > r) xb = cfma(A[(kb + tt) * LDA + kb + r], A[(kb + tt) * LDA + R + c], xb);
           }
+          __syncwarp();
+          if (lane < 24) A[(kb + r) * LDA + R + c] = xb;
+          __syncwarp();
+          for (int task = lane; task < kb * 3; task += 32) {
+            const int i = task / 3, cc = task - 3 * i;
+            double2 acc = A[i * LDA + R + cc];
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) acc = cfms(A[i * LDA + kb + tt], A[(kb + tt) * LDA + R + cc], acc);
+            A[i * LDA + R + cc] = acc;
+          }
+          __syncwarp();
+        }
+        for (int e = lane; e < 3 * R; e += 32) {
+          const int c = e / R, i = e - c * R;
+          Pw[e] = A[i * LDA + R + c];
+          if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = A[i * LDA + R + c];
         }
       } else {
-        for (int i = lane; i < R; i += 32) Pw[c * R + i] = make_double2(nanv, nanv);
+        for (int e = lane; e < 3 * R; e += 32) Pw[e] = make_double2(nanv, nanv);
         if (a.P_out)
-          for (int i = lane; i < a.r; i += 32)
-            reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = make_double2(nanv, nanv);
+          for (int e = lane; e < 3 * a.r; e += 32)
+            reinterpret_cast<double2 *>(a.P_out)[(size_t)t * 3 * a.r + e] = make_double2(nanv, nanv);
       }
     }
     LB_TR(3);

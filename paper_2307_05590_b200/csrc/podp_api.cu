@@ -410,7 +410,7 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
       if (!tr[0]) continue;
       fprintf(stderr, "omega %d: assembled %lld, LU done %lld, back-sub done %lld\n", q, tr[1] - tr[0], tr[2] - tr[0], tr[3] - tr[0]);
       for (int k = 0; k < 16 && tr[16 + 4 * k]; ++k)
-        fprintf(stderr, "  panel %d: start %lld  swaps/U12 %lld  trailing %lld\n", k, tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0]);
+        fprintf(stderr, "  panel %d: passed hand-off %lld  after lookahead %lld  after own tiles %lld\n", k, tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0]);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");
