@@ -55,8 +55,13 @@ enum {
   PODP_FLAG_DEFAULT = 0,        /* first output = Rt = N0 + R                                              */
   PODP_FLAG_OUT_R = 1u << 0,    /* first output = omega-dependent R only (used by parity runs, reading U11)  */
   PODP_FLAG_OUT_P = 1u << 1,    /* debug: also write P (n_obj x F x 3 x r complex, row-major) to P_d       */
-  PODP_FLAG_NO_PIVOT = 1u << 2  /* LU without pivoting (exists since Re x^H A x = x^H K x > 0 for K > 0;
+  PODP_FLAG_NO_PIVOT = 1u << 2, /* LU without pivoting (exists since Re x^H A x = x^H K x > 0 for K > 0;
                                    SURVEY Appendix A.4).  Default is partial pivoting.                       */
+  PODP_FLAG_PENCIL = 1u << 3    /* NEXT row N3: solve with the pencil reduction precomputed by
+                                   podp_create (K = L L^H, L^{-1} M L^{-H} = V Lambda V^H, Z = L^{-H} V), i.e.
+                                   P = Z (I + i omega nu Lambda)^{-1} Z^H B(omega): O(r^2) per frequency instead of
+                                   the LU's O(r^3).  Exact in exact arithmetic; requires K positive definite
+                                   (PODP_ERR_UNSUPPORTED otherwise).  R, I, Delta are then formed as usual. */
 };
 
 /* Operators of ONE object (host pointers; copied, validated and packed by podp_create; caller keeps ownership).

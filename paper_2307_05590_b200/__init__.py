@@ -3,6 +3,6 @@
 The product is libpodp.so (C ABI, include/podp.h) built from ``csrc/``; ``podp`` is its thin ctypes binding.
 """
 from .podp import (  # noqa: F401
-    Evaluator, PodpError, load_library, LIB_PATH, EXPORTED, FLAG_DEFAULT, FLAG_OUT_R, FLAG_OUT_P, FLAG_NO_PIVOT,
+    Evaluator, PodpError, load_library, LIB_PATH, EXPORTED, FLAG_DEFAULT, FLAG_OUT_R, FLAG_OUT_P, FLAG_NO_PIVOT, FLAG_PENCIL,
     R_MAX, STATUS_NAMES, profile_enable, profile_read,
 )

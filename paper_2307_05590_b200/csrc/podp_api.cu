@@ -11,6 +11,7 @@
 #include "podp_internal.h"
 
 struct podp_ctx {
+  bool pencil_ok;      // pencil precompute available (K positive definite for every object)
   int device;
   int r;
   int n_obj;
@@ -171,6 +172,19 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   }
   double *sc = dst + L.scal;
   sc[podp::SC_NU] = o.nu;
+  sc[podp::SC_PENCIL_OK] = 0.0;
+  if (R == r) {
+    std::vector<double> Z, lam, c0, c1;
+    if (podp::pencil_precompute(r, o.K, o.M, o.b0, o.b1, Z, lam, c0, c1)) {
+      for (size_t e = 0; e < Z.size(); ++e) dst[L.Z + e] = Z[e];
+      for (int e = 0; e < r; ++e) dst[L.lam + e] = lam[e];
+      for (size_t e = 0; e < c0.size(); ++e) {
+        dst[L.c0 + e] = c0[e];
+        dst[L.c1 + e] = c1[e];
+      }
+      sc[podp::SC_PENCIL_OK] = 1.0;
+    }
+  }
   sc[podp::SC_ALPHA] = o.alpha;
   sc[podp::SC_ALPHA_LB] = o.alpha_lb;
   for (int e = 0; e < 9; ++e) {
@@ -207,6 +221,10 @@ Layout make_layout(int R) {
   L.GbM = take(vec6);
   L.Gbb = take(72);
   L.scal = take(SCAL_N);
+  L.Z = take(sq);
+  L.lam = take(R);
+  L.c0 = take(vec3);
+  L.c1 = take(vec3);
   L.stride = off;
   return L;
 }
@@ -271,6 +289,8 @@ podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int devi
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   podp_ctx *c = new podp_ctx;
+  c->pencil_ok = true;
+  for (int k = 0; k < n_obj; ++k) c->pencil_ok &= host[(size_t)L.stride * k + L.scal + podp::SC_PENCIL_OK] == 1.0;
   c->pool = pool;
   c->device = device;
   c->r = r;
@@ -341,7 +361,9 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   if (F == 0) return PODP_OK;
   if (!omega_d || !T1_d || !I_d || !Delta_d) return fail(PODP_ERR_ARG, "null omega/output pointer");
   if ((flags & PODP_FLAG_OUT_P) && !P_d) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P set but P_d is NULL");
-  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_INTERNAL_FORCE_GENERIC)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
+  if ((flags & PODP_FLAG_PENCIL) && !c->pencil_ok)
+    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_PENCIL needs K Hermitian positive definite (Cholesky failed)");
+  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_FLAG_PENCIL | PODP_INTERNAL_FORCE_GENERIC)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
   DeviceGuard guard(c->device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -373,7 +395,8 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   {
     ProfScope ps("solve", s);
     const char *lv = getenv("PODP_LU_IMPL");  // dev switch: "reg" = register-resident kernel, default blocked
-    if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
+    if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
+    else if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
     else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
     else if (lv && lv[0] == 'p') e = podp::launch_lu_pw(a, s);
     else e = podp::launch_lu_blk(a, s);

@@ -1,6 +1,7 @@
 // Internal declarations shared by the libpodp translation units (not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 #include "podp.h"
 
@@ -16,10 +17,11 @@ struct Layout {
   int64_t GbK, GbM;               // 6 x R complex (row a = b-slot a)
   int64_t Gbb;                    // 6 x 6 complex
   int64_t scal;                   // SCAL_N doubles (see below)
+  int64_t Z, lam, c0, c1;         // pencil precompute (N3): Z (R x R complex), lambda (R), c0, c1 (3 x R complex)
   int64_t stride;                 // doubles per object (multiple of 32)
 };
 
-enum { SC_NU = 0, SC_ALPHA = 1, SC_ALPHA_LB = 2, SC_S = 4, SC_N0 = 13, SCAL_N = 32 };
+enum { SC_NU = 0, SC_ALPHA = 1, SC_ALPHA_LB = 2, SC_PENCIL_OK = 3, SC_S = 4, SC_N0 = 13, SCAL_N = 32 };
 
 Layout make_layout(int R);
 
@@ -46,6 +48,10 @@ cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNot
 cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_lu_pw(const EvalArgs &a, cudaStream_t s);     // cudaErrorNotSupported if no instantiation
+cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
+bool pencil_precompute(int r, const double *K, const double *M, const double *b0, const double *b1,
+                       std::vector<double> &Z, std::vector<double> &lam, std::vector<double> &c0,
+                       std::vector<double> &c1);
 cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch);
 // bytes of global scratch launch_solve needs for this R (0 if the shared-memory variant fits)
 size_t solve_scratch_bytes(int R, int sms);

@@ -280,3 +280,36 @@ def test_full_size_configs_sampled(torch_cuda, cfg):
         ow, oidx, oLam, _ = oracle.select(omega, out["Delta"][0].cpu().numpy(), c["snap"], 2)
         assert list(idx) == oidx and Lam == oLam
     ev.close()
+
+
+@pytest.mark.parametrize("r,F", [(8, 200), (24, 500), (48, 333), (96, 61), (32, 129)])
+def test_pencil_solver_parity(torch_cuda, r, F):
+    """NEXT row N3: the pencil reformulation (P = Z (I + i omega nu Lambda)^{-1} Z^H B) matches the LU oracle."""
+    from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_PENCIL
+    ops = g.make_config0()[0] if r == 8 else g.make_operators(r)
+    omega = g.omega_grid(F)
+    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_PENCIL, want_P=True)
+    assert (res["info"] == 0).all()
+    check_parity(ops, omega, res)
+    for f in range(0, F, max(1, F // 13)):
+        Po = solve_reduced(ops.K, ops.M, ops.b0, ops.b1, ops.nu, float(omega[f]))
+        assert np.linalg.norm(res["P"][0, f].T - Po) / np.linalg.norm(Po) <= 1e-10
+
+
+def test_pencil_batch_and_unsupported(torch_cuda):
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R, FLAG_PENCIL, PodpError
+    sig = g.batch_sigma(256)
+    ops = [g.make_operators(32, seed=k, nu=g.MU0 * sig[k] * 1e-4) for k in range(4)]
+    omega = g.omega_grid(77)
+    res = run_gpu(torch, ops, omega, flags=FLAG_OUT_R | FLAG_PENCIL)
+    for k in range(4):
+        check_parity(ops[k], omega, res, obj=k, sample=range(0, 77, 5))
+    # K not positive definite -> the pencil path is refused (the LU path still works)
+    o = g.make_operators(8)
+    o = g.Operators(**{**o.__dict__, "K": o.K - 20.0 * np.eye(8)})
+    ev = Evaluator(o)
+    with pytest.raises(PodpError) as ei:
+        ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_PENCIL)
+    assert ei.value.status == 4
+    ev.close()
