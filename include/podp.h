@@ -126,6 +126,17 @@ podp_status podp_select(const podp_ctx *ctx, const double *omega_d, const double
                         double *omega_new, int64_t *idx_new, double *Lambda, double *Lambda_n,
                         void *cuda_stream);
 
+/* NEXT row N4 -- per-frequency epilogues on podp_eval outputs (device buffers, asynchronous):
+ *   podp_invariants: eigenvalues of Rt (first output) and of I, ascending, n x 3 doubles each -- the rotation
+ *     invariants used for dictionary matching.  n = number of output rows (n_obj * F).
+ *   podp_coil_voltage: V_c = (H0^ms_c)_i (Rt + i I)_ij (H0_c)_j for n_coil coil pairs (eqn:meas_voltage,
+ *     P:393-395).  h_ex, h_ms: host, n_coil x 3 real background fields at the object; V_d: device, n x n_coil
+ *     complex (interleaved re, im).  1 <= n_coil <= 64.  Synchronous w.r.t. the small host->device copy only. */
+podp_status podp_invariants(const double *T1_d, const double *I_d, int64_t n, double *eigR_d, double *eigI_d,
+                            void *cuda_stream);
+podp_status podp_coil_voltage(const double *T1_d, const double *I_d, int64_t n, const double *h_ex,
+                              const double *h_ms, int32_t n_coil, double *V_d, void *cuda_stream);
+
 /* Number of objects / modes of a context (0 if ctx is NULL). */
 int32_t podp_n_obj(const podp_ctx *ctx);
 int32_t podp_r(const podp_ctx *ctx);

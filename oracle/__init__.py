@@ -20,5 +20,5 @@ evaluates the formula only.
 """
 from .podp_oracle import (  # noqa: F401
     ENTRY_ORDER, solve_reduced, mpt_R, mpt_I, residual_coeffs, certificate, evaluate_one, evaluate, select,
-    to6, from6,
+    to6, from6, invariants, coil_voltage,
 )

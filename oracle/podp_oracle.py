@@ -174,3 +174,22 @@ def select(omegas, Delta6, snap, n_star: int, theta: float | None = None):
     order = sorted(cands, key=lambda t: (-lam[t], t))[:n_star]
     idx = sorted(arg[t] for t in order)
     return [float(omegas[f]) for f in idx], idx, Lam, lam
+
+
+def invariants(T6) -> tuple:
+    """Rotation invariants of the MPT: ascending eigenvalues of Rt and of I (numpy.linalg.eigvalsh on the
+    3x3 symmetric blocks).  T6: (n, 6) pair (Rt6, I6).  Returns (n x 3, n x 3)."""
+    R6, I6 = T6
+    eR = np.array([np.linalg.eigvalsh(from6(r)) for r in R6])
+    eI = np.array([np.linalg.eigvalsh(from6(i)) for i in I6])
+    return eR, eI
+
+
+def coil_voltage(Rt6, I6, h_ex, h_ms):
+    """eqn:meas_voltage: V = (H0^ms)_i M_ij (H0)_j with M = Rt + i I.  Returns (n, n_coil) complex."""
+    out = np.zeros((len(Rt6), len(h_ex)), dtype=np.complex128)
+    for f in range(len(Rt6)):
+        Mx = from6(Rt6[f]) + 1j * from6(I6[f])
+        for c in range(len(h_ex)):
+            out[f, c] = np.asarray(h_ms[c]) @ Mx @ np.asarray(h_ex[c])
+    return out

@@ -305,6 +305,38 @@ podp_status podp_create(const podp_operators *ops, int device, void *cuda_stream
   return podp_create_batch(1, ops, device, cuda_stream, out);
 }
 
+podp_status podp_invariants(const double *T1_d, const double *I_d, int64_t n, double *eigR_d, double *eigI_d,
+                            void *cuda_stream) {
+  g_err.clear();
+  if (n < 0) return fail(PODP_ERR_ARG, "n < 0");
+  if (n == 0) return PODP_OK;
+  if (!T1_d || !I_d || !eigR_d || !eigI_d) return fail(PODP_ERR_ARG, "null pointer");
+  cudaError_t e = podp::launch_invariants(T1_d, I_d, n, eigR_d, eigI_d, (cudaStream_t)cuda_stream);
+  if (e != cudaSuccess) return cuda_fail(e, "podp_invariants");
+  return PODP_OK;
+}
+
+podp_status podp_coil_voltage(const double *T1_d, const double *I_d, int64_t n, const double *h_ex,
+                              const double *h_ms, int32_t n_coil, double *V_d, void *cuda_stream) {
+  g_err.clear();
+  if (n < 0) return fail(PODP_ERR_ARG, "n < 0");
+  if (n_coil < 1 || n_coil > 64) return fail(PODP_ERR_ARG, "need 1 <= n_coil <= 64");
+  if (!h_ex || !h_ms) return fail(PODP_ERR_ARG, "null coil field pointer");
+  if (n == 0) return PODP_OK;
+  if (!T1_d || !I_d || !V_d) return fail(PODP_ERR_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  double *h = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&h, sizeof(double) * 6 * n_coil, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(coil fields)");
+  e = cudaMemcpyAsync(h, h_ex, sizeof(double) * 3 * n_coil, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h + 3 * n_coil, h_ms, sizeof(double) * 3 * n_coil, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = podp::launch_coil_voltage(T1_d, I_d, n, h, h + 3 * n_coil, n_coil, V_d, s);
+  cudaFreeAsync(h, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host arrays may be released by the caller
+  if (e != cudaSuccess) return cuda_fail(e, "podp_coil_voltage");
+  return PODP_OK;
+}
+
 podp_status podp_profile_enable(int on) {
   g_prof_on = on != 0;
   return PODP_OK;

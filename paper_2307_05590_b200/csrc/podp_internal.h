@@ -49,6 +49,9 @@ cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s);  // cudaErrorNot
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_lu_pw(const EvalArgs &a, cudaStream_t s);     // cudaErrorNotSupported if no instantiation
 cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
+cudaError_t launch_invariants(const double *T1, const double *I, int64_t n, double *eigR, double *eigI, cudaStream_t s);
+cudaError_t launch_coil_voltage(const double *T1, const double *I, int64_t n, const double *hex_d, const double *hms_d,
+                                int n_coil, double *V, cudaStream_t s);
 bool pencil_precompute(int r, const double *K, const double *M, const double *b0, const double *b1,
                        std::vector<double> &Z, std::vector<double> &lam, std::vector<double> &c0,
                        std::vector<double> &c1);

@@ -26,7 +26,7 @@ STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ER
                 5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}
 EXPORTED = ["podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
             "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version", "podp_profile_enable",
-            "podp_profile_read"]
+            "podp_profile_read", "podp_invariants", "podp_coil_voltage"]
 
 
 class PodpError(RuntimeError):
@@ -69,6 +69,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.podp_r.restype = i32
     lib.podp_last_launch_count.restype = i32
     lib.podp_last_error.restype = ctypes.c_char_p
+    lib.podp_invariants.argtypes = [P, P, i64, P, P, P]
+    lib.podp_invariants.restype = ctypes.c_int
+    lib.podp_coil_voltage.argtypes = [P, P, i64, P, P, i32, P, P]
+    lib.podp_coil_voltage.restype = ctypes.c_int
     lib.podp_profile_enable.argtypes = [ctypes.c_int]
     lib.podp_profile_enable.restype = ctypes.c_int
     lib.podp_profile_read.argtypes = [P, P, P, i32, i32]
@@ -96,6 +100,45 @@ def profile_read(reset: bool = True) -> dict:
         nm = names.raw[32 * i:32 * (i + 1)].split(b"\0")[0].decode()
         out[nm] = (float(ms[i]), int(cnt[i]))
     return out
+
+
+def invariants(T1, I, stream=None):
+    """NEXT row N4: eigenvalues (ascending) of Rt and I per output row.  T1, I: (..., 6) float64 CUDA
+    tensors from Evaluator.eval.  Returns (eigR, eigI) of shape (..., 3)."""
+    import torch
+    T1c, Ic = T1.contiguous(), I.contiguous()
+    n = T1c.numel() // 6
+    eR = torch.empty(T1c.shape[:-1] + (3,), dtype=torch.float64, device=T1c.device)
+    eI = torch.empty_like(eR)
+    _check(load_library().podp_invariants(ctypes.c_void_p(T1c.data_ptr()), ctypes.c_void_p(Ic.data_ptr()), n,
+                                          ctypes.c_void_p(eR.data_ptr()), ctypes.c_void_p(eI.data_ptr()),
+                                          _stream_handle(stream)))
+    return eR, eI
+
+
+def coil_voltage(T1, I, h_ex, h_ms, stream=None):
+    """NEXT row N4: V = h_ms^T (Rt + i I) h_ex for each coil pair (eqn:meas_voltage).
+    h_ex, h_ms: (n_coil, 3) real background fields at the object.  Returns complex128 (..., n_coil)."""
+    import torch
+    h_ex = np.ascontiguousarray(h_ex, dtype=np.float64).reshape(-1, 3)
+    h_ms = np.ascontiguousarray(h_ms, dtype=np.float64).reshape(-1, 3)
+    if h_ex.shape != h_ms.shape:
+        raise ValueError("h_ex and h_ms must have the same shape (n_coil, 3)")
+    T1c, Ic = T1.contiguous(), I.contiguous()
+    n = T1c.numel() // 6
+    V = torch.empty(T1c.shape[:-1] + (h_ex.shape[0],), dtype=torch.complex128, device=T1c.device)
+    _check(load_library().podp_coil_voltage(ctypes.c_void_p(T1c.data_ptr()), ctypes.c_void_p(Ic.data_ptr()), n,
+                                            ctypes.c_void_p(h_ex.ctypes.data), ctypes.c_void_p(h_ms.ctypes.data),
+                                            h_ex.shape[0], ctypes.c_void_p(V.data_ptr()), _stream_handle(stream)))
+    return V
+
+
+def scale_signature(omega, outputs: dict, s: float) -> tuple:
+    """Remark 6.2: M[s alpha B, omega] = s^3 M[alpha B, s^2 omega].  Given a signature evaluated on
+    the grid `omega` for object alpha B, returns the grid omega / s^2 and the outputs scaled by s^3 for the
+    scaled object s alpha B -- a dictionary entry at zero extra solves (NEXT row N4)."""
+    f = float(s) ** 3
+    return omega / float(s) ** 2, {k: (v * f if k in ("T1", "I", "Delta") else v) for k, v in outputs.items()}
 
 
 def _check(st: int):

@@ -313,3 +313,27 @@ def test_pencil_batch_and_unsupported(torch_cuda):
         ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_PENCIL)
     assert ei.value.status == 4
     ev.close()
+
+
+def test_N4_invariants_and_voltage_parity(torch_cuda):
+    torch = torch_cuda
+    import paper_2307_05590_b200 as pb
+    ops = g.make_operators(24)
+    omega = g.omega_grid(301)
+    ev = pb.Evaluator(ops)
+    out = ev.eval(torch.tensor(omega, device="cuda"))
+    eR, eI = pb.invariants(out["T1"], out["I"])
+    T1, I = out["T1"][0].cpu().numpy(), out["I"][0].cpu().numpy()
+    oR, oI = oracle.invariants((T1, I))
+    for gpu, ora in ((eR[0].cpu().numpy(), oR), (eI[0].cpu().numpy(), oI)):
+        scale = np.abs(ora).max(axis=1, keepdims=True)
+        assert np.max(np.abs(gpu - ora) / scale) <= 1e-13
+    rng = np.random.default_rng(0)
+    hx, hm = rng.standard_normal((5, 3)), rng.standard_normal((5, 3))
+    V = pb.coil_voltage(out["T1"], out["I"], hx, hm)[0].cpu().numpy()
+    Vo = oracle.coil_voltage(T1, I, hx, hm)
+    assert np.max(np.abs(V - Vo) / np.abs(Vo).max()) <= 1e-14
+    # Remark 6.2 relabelling helper is exact
+    om2, sc = pb.scale_signature(omega, {"T1": out["T1"], "I": out["I"], "Delta": out["Delta"]}, 2.0)
+    assert np.array_equal(om2, omega / 4.0) and torch.equal(sc["I"], 8.0 * out["I"])
+    ev.close()

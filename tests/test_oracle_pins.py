@@ -321,3 +321,37 @@ def test_C12_bruteforce_and_conventions():
     assert i3 == [4, 5]
     with pytest.raises(ValueError):
         oracle.select(om2, D2, snap2, 3)
+
+
+# ---------------------------------------------------------------- N4 epilogues (invariants, coil voltage)
+def test_N4_invariants_pins():
+    rng = np.random.default_rng(4)
+    # isotropic m I -> (m, m, m)
+    R6 = np.array([[2.0, 2.0, 2.0, 0, 0, 0]])
+    eR, eI = oracle.invariants((R6, R6))
+    assert np.array_equal(eR, [[2.0, 2.0, 2.0]])
+    # trace and determinant identities, rotation invariance
+    for _ in range(5):
+        X = rng.standard_normal((3, 3)); T = X + X.T
+        Q, _r = np.linalg.qr(rng.standard_normal((3, 3)))
+        e1, _ = oracle.invariants((np.array([oracle.to6(T)]), np.array([oracle.to6(T)])))
+        e2, _ = oracle.invariants((np.array([oracle.to6(Q @ T @ Q.T)]),) * 2)
+        assert abs(e1.sum() - np.trace(T)) < 1e-12 and abs(np.prod(e1) - np.linalg.det(T)) < 1e-11
+        assert np.allclose(e1, e2, atol=1e-12)
+    # block structure: (1,2)-coupled block + isolated (3,3) entry -> that entry is an eigenvalue
+    T = np.array([[1.0, 0.5, 0], [0.5, 2.0, 0], [0, 0, 7.0]])
+    e, _ = oracle.invariants((np.array([oracle.to6(T)]),) * 2)
+    assert np.isclose(e[0], 7.0).any()
+
+
+def test_N4_voltage_pins():
+    rng = np.random.default_rng(5)
+    R6 = rng.standard_normal((4, 6)); I6 = rng.standard_normal((4, 6))
+    hx = rng.standard_normal((3, 3)); hm = rng.standard_normal((3, 3))
+    V = oracle.coil_voltage(R6, I6, hx, hm)
+    assert np.allclose(V, oracle.coil_voltage(R6, I6, hm, hx))           # reciprocity (M symmetric)
+    assert np.array_equal(oracle.coil_voltage(0 * R6, 0 * I6, hx, hm), np.zeros((4, 3)))  # M = 0 -> V = 0
+    # diagonal M, axis-aligned fields: V = M_kk (h_ms)_k (h_ex)_k
+    Rd = np.array([[1.0, 2.0, 3.0, 0, 0, 0]]); Id = np.array([[0.5, 0.0, -1.0, 0, 0, 0]])
+    v = oracle.coil_voltage(Rd, Id, [[0, 0, 2.0]], [[0, 0, 3.0]])
+    assert v[0, 0] == (3.0 - 1.0j) * 6.0
