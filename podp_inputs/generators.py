@@ -244,3 +244,53 @@ def make_config(k: int, F: int | None = None, n_obj: int | None = None):
     if k == 4:
         out["snap"] = snapshot_grid(spec["n_snap"])
     return out
+
+
+@dataclasses.dataclass
+class FullOrderSystem:
+    """Synthetic full-order system for the Algorithm-1 driver (NEXT row N2).
+
+    (K_full + i omega nu M_full) q_i = B0f_i + omega B1f_i  (eqn:Linear P:476-483, BASELINE sign), C_full = nu M_full,
+    v: N x 3 real conductor coefficients (theta0-tilde + e_i x xi), so S = v^T C v and H = v^T C U."""
+    K_full: np.ndarray
+    M_full: np.ndarray
+    C_full: np.ndarray
+    v: np.ndarray
+    B0f: np.ndarray
+    B1f: np.ndarray
+    nu: float
+    alpha: float
+    alpha_lb: float
+
+    @property
+    def N(self) -> int:
+        return int(self.K_full.shape[0])
+
+
+def make_fullorder(seed: int = 0, N: int = 1000, n_modes: int = 120, w_lo: float = 1e2, w_hi: float = 1e7,
+                   b0_scale: float = 0.1, nu: float = NU_DEFAULT, alpha: float = ALPHA_DEFAULT,
+                   alpha_lb: float = 0.1) -> FullOrderSystem:
+    """Full-order recipe with the spectral structure of an MPT signature (sum of first-order relaxation terms,
+    Lemma 8.5 / P:928): K_full = A^H A + 0.1 I (A sparse, 8 CN(0,1) entries per row), M_full = X diag(lam) X^H of
+    rank n_modes supported on the conductor half, lam log-spaced so the relaxation frequencies 1/(nu lam) fall in
+    [w_lo, w_hi]; B1f = -i nu M_full v (the source is omega times the conductor term, so q -> -v as omega -> inf,
+    P:437 with the omega-free nu); B0f = b0_scale CN(0,1) (the omega-independent mu_r-contrast term).
+    Draw order: (1) A columns, (2) A values, (3) X, (4) v, (5) B0f."""
+    rng = np.random.default_rng(seed)
+    nnz_per_row = 8
+    cols = rng.integers(0, N, nnz_per_row * N)
+    vals = cn(rng, (nnz_per_row * N,), 1.0)
+    A = np.zeros((N, N), dtype=np.complex128)
+    np.add.at(A, (np.repeat(np.arange(N), nnz_per_row), cols), vals)
+    K_full = _herm(A.conj().T @ A + 0.1 * np.eye(N))
+    Nc = N // 2
+    X = np.zeros((N, n_modes), dtype=np.complex128)
+    X[:Nc] = cn(rng, (Nc, n_modes), 1.0 / Nc)
+    lam = np.logspace(math.log10(1.0 / (nu * w_lo)), math.log10(1.0 / (nu * w_hi)), n_modes)
+    M_full = _herm((X * lam) @ X.conj().T)
+    v = np.zeros((N, 3))
+    v[:Nc] = rng.standard_normal((Nc, 3))
+    B0f = b0_scale * cn(rng, (N, 3), 1.0)
+    B1f = -1j * nu * (M_full @ v)
+    return FullOrderSystem(K_full=K_full, M_full=M_full, C_full=nu * M_full, v=v, B0f=B0f, B1f=B1f, nu=float(nu),
+                           alpha=float(alpha), alpha_lb=float(alpha_lb))

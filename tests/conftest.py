@@ -25,3 +25,12 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def torch_cuda():
+    """Builds libpodp.so in-tree (sm_100a) and returns torch; GPU tests only."""
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    return torch

@@ -13,14 +13,6 @@ import podp_inputs as g
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def torch_cuda():
-    import torch
-    import __graft_entry__
-    __graft_entry__.build()
-    return torch
-
-
 def run_gpu(torch, ops, omega, flags=None, want_P=False, device=0):
     from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
     ev = Evaluator(ops, device=device)
