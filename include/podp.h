@@ -81,6 +81,12 @@ typedef struct {
   const double *H;      /* 3 x r complex: row i = h_i = o_i^T C2 U + t_i^T U (unconjugated)           */
   const double *G;      /* (6+2r) x (6+2r) complex Hermitian PSD Gram of the residual factor, slot order
                            [b0_1, b1_1, b0_2, b1_2, b0_3, b1_3 | K U (r) | M U (r)]  (reading U9)     */
+  const double *M_I;    /* r x r complex Hermitian, or NULL (= M): conductor mass used in I only.  The paper's
+                           per-direction form (NEXT row N1; U_i^M per direction) is the
+                           embedding U = [U_1 U_2 U_3] (r = M_1+M_2+M_3) with K, M block-diagonal (A_i^M blocks,
+                           P:596), b0/b1 column i nonzero only in block i, K_R = [K_ij^M], M_I = [C_ij^M]/nu
+                           (P:618), H row i = [o_i^T C2 U_j + t_i U_j]_j and G the Gram of
+                           [B0_1, B1_1, ..., B1_3 | K U | M U]; then column i of P is (0, p_i^M, 0).         */
 } podp_operators;
 
 /* Validate + pack one object's operators onto `device`; the upload is enqueued on cuda_stream and complete

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from .perdir import PerDirectionROM, tsvd_per_direction
 from .podp_oracle import evaluate, select
 
 
@@ -49,7 +50,8 @@ def reduced_operators(fom, U: np.ndarray):
 
 
 def run_adaptive(fom, omegas, n0: int = 13, n_star: int = 2, tol_sigma: float = 1e-6, tol_delta: float = 1e-3,
-                 max_k: int = 4, vol: float = 1.0, theta: float | None = None, snap0=None):
+                 max_k: int = 4, vol: float = 1.0, theta: float | None = None, snap0=None,
+                 per_direction: bool = False):
     """Algorithm 1 lines 1-26.  Returns (ops, (T1, I, Delta) on omegas, history) where history[k-1] =
     dict(k, N, r, Lambda, snap (sorted), new (omegas chosen at this k, empty at the last))."""
     from podp_inputs.generators import snapshot_grid
@@ -58,12 +60,19 @@ def run_adaptive(fom, omegas, n0: int = 13, n_star: int = 2, tol_sigma: float = 
     k = 1
     history = []
     while True:
-        D = np.concatenate([Q[w] for w in snap], axis=1)                                 # lines 5 / 18
-        U = tsvd(D, tol_sigma)                                                           # lines 6 / 19
-        ops = reduced_operators(fom, U)
-        T1, I, Dl = evaluate(ops, omegas)                                                # line 11
+        if per_direction:                                                                # N1: D_i, U_i^M
+            Us = tsvd_per_direction([Q[w] for w in snap], tol_sigma)
+            ops = PerDirectionROM(fom, Us)
+            T1, I, Dl = ops.evaluate(omegas)
+            m = [U.shape[1] for U in Us]
+        else:
+            D = np.concatenate([Q[w] for w in snap], axis=1)                             # lines 5 / 18
+            U = tsvd(D, tol_sigma)                                                       # lines 6 / 19
+            ops = reduced_operators(fom, U)
+            T1, I, Dl = evaluate(ops, omegas)                                            # line 11
+            m = [U.shape[1]]
         new, _idx, Lam, _lam = select(omegas, Dl, snap, n_star, theta)                   # lines 12-15
-        rec = dict(k=k, N=len(snap), r=U.shape[1], Lambda=Lam, snap=list(snap), new=[])
+        rec = dict(k=k, N=len(snap), r=sum(m), m=m, Lambda=Lam, snap=list(snap), new=[])
         history.append(rec)
         if not (Lam / vol > tol_delta and k < max_k):                                    # line 8
             return ops, (T1, I, Dl), history

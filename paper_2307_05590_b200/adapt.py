@@ -38,6 +38,7 @@ class ReducedOperators:
     alpha: float
     alpha_lb: float
     K_R: np.ndarray | None = None
+    M_I: np.ndarray | None = None
 
     @property
     def r(self) -> int:
@@ -91,6 +92,24 @@ class FullOrderGPU:
                                 alpha=self.alpha, alpha_lb=self.alpha_lb)
 
 
+    def reduce_per_direction(self, Us) -> ReducedOperators:
+        """NEXT row N1: per-direction bases U_i (N x M_i) in the block embedding of perdir.py: U = [U_1 U_2 U_3],
+        K, M block-diagonal (the three A_i^M), K_R = [K_ij^M], M_I = [C_ij^M]/nu, b column i
+        restricted to block i; G is then the Gram of [B0_1, B1_1, ... | K U | M U] as in the shared form."""
+        import torch
+        m = [int(U.shape[1]) for U in Us]
+        U = torch.cat(list(Us), dim=1)
+        full = self.reduce(U)
+        off = np.concatenate([[0], np.cumsum(m)])
+        blk = np.zeros((full.r, full.r), dtype=bool)
+        rows = np.zeros((full.r, 3), dtype=bool)
+        for i in range(3):
+            blk[off[i]:off[i + 1], off[i]:off[i + 1]] = True
+            rows[off[i]:off[i + 1], i] = True
+        return dataclasses.replace(full, K=np.where(blk, full.K, 0), M=np.where(blk, full.M, 0), K_R=full.K,
+                                   M_I=full.M, b0=np.where(rows, full.b0, 0), b1=np.where(rows, full.b1, 0))
+
+
 def tsvd(D, tol_sigma: float):
     """Lines 6 / 19: D^M = U^M Sigma^M (V^M)^H, keeping s_k / s_1 >= TOL_Sigma."""
     import torch
@@ -101,7 +120,7 @@ def tsvd(D, tol_sigma: float):
 
 def run_adaptive(fom, omegas, n0: int = 13, n_star: int = 2, tol_sigma: float = 1e-6, tol_delta: float = 1e-3,
                  max_k: int = 4, vol: float = 1.0, theta: float | None = None, snap0=None, device: int = 0,
-                 flags: int = 0):
+                 flags: int = 0, per_direction: bool = False):
     """Algorithm 1 lines 1-26 with the certification on `omegas` (the output grid / adaption window).
 
     Returns (ops, outputs dict(T1, I, Delta) of the final ROM on omegas (device tensors, n_obj = 1), history) where
@@ -116,9 +135,15 @@ def run_adaptive(fom, omegas, n0: int = 13, n_star: int = 2, tol_sigma: float = 
     history = []
     t0 = time.perf_counter()
     while True:
-        D = torch.cat([Q[w] for w in snap], dim=1)                                        # lines 5 / 18
-        U = tsvd(D, tol_sigma)                                                            # lines 6 / 19
-        ops = g.reduce(U)
+        if per_direction:                                                                 # N1: D_i, U_i^M
+            Us = [tsvd(torch.stack([Q[w][:, i] for w in snap], dim=1), tol_sigma) for i in range(3)]
+            ops = g.reduce_per_direction(Us)
+            m = [int(U.shape[1]) for U in Us]
+        else:
+            D = torch.cat([Q[w] for w in snap], dim=1)                                    # lines 5 / 18
+            U = tsvd(D, tol_sigma)                                                        # lines 6 / 19
+            ops = g.reduce(U)
+            m = [ops.r]
         torch.cuda.synchronize(g.dev)
         t1 = time.perf_counter()
         ev = Evaluator(ops, device=g.dev.index)
@@ -127,7 +152,7 @@ def run_adaptive(fom, omegas, n0: int = 13, n_star: int = 2, tol_sigma: float = 
                                          0.0 if theta is None else theta)                 # lines 12-15
         ev.close()
         t2 = time.perf_counter()
-        rec = dict(k=k, N=len(snap), r=ops.r, Lambda=float(Lam), snap=list(snap), new=[], t_offline=t1 - t0,
+        rec = dict(k=k, N=len(snap), r=ops.r, m=m, Lambda=float(Lam), snap=list(snap), new=[], t_offline=t1 - t0,
                    t_online=t2 - t1)
         history.append(rec)
         if not (Lam / vol > tol_delta and k < max_k):                                     # line 8

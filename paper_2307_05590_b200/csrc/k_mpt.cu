@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NW * 32) mpt_simple_kernel(EvalArgs a) {
       continue;
     }
     const double2 *KR = reinterpret_cast<const double2 *>(op + a.L.KR);
-    const double2 *Mm = reinterpret_cast<const double2 *>(op + a.L.M);
+    const double2 *Mm = reinterpret_cast<const double2 *>(op + a.L.MI);
     const double2 *Gkk = reinterpret_cast<const double2 *>(op + a.L.Gkk);
     const double2 *Jm = reinterpret_cast<const double2 *>(op + a.L.J);
     const double2 *Gmm = reinterpret_cast<const double2 *>(op + a.L.Gmm);

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
         __syncthreads();
         const double *opl = a.ops + (size_t)obj0 * a.L.stride;
         const double2 *gKR = reinterpret_cast<const double2 *>(opl + a.L.KR);
-        const double2 *gM = reinterpret_cast<const double2 *>(opl + a.L.M);
+        const double2 *gM = reinterpret_cast<const double2 *>(opl + a.L.MI);
         const double2 *gGk = reinterpret_cast<const double2 *>(opl + a.L.Gkk);
         const double2 *gJ = reinterpret_cast<const double2 *>(opl + a.L.J);
         const double2 *gGm = reinterpret_cast<const double2 *>(opl + a.L.Gmm);
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
       // operators for this frequency: shared-memory block (tile of one object) or global (mixed tile)
       const bool shared_ops = one_obj;
       const double2 *oKR = shared_ops ? sKR : reinterpret_cast<const double2 *>(op + a.L.KR) + a0 * R;
-      const double2 *oM = shared_ops ? sM : reinterpret_cast<const double2 *>(op + a.L.M) + a0 * R;
+      const double2 *oM = shared_ops ? sM : reinterpret_cast<const double2 *>(op + a.L.MI) + a0 * R;
       const double2 *oGk = shared_ops ? sGk : reinterpret_cast<const double2 *>(op + a.L.Gkk) + a0 * R;
       const double2 *oJ = shared_ops ? sJ : reinterpret_cast<const double2 *>(op + a.L.J) + a0 * R;
       const double2 *oGm = shared_ops ? sGm : reinterpret_cast<const double2 *>(op + a.L.Gmm) + a0 * R;

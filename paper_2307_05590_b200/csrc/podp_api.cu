@@ -119,13 +119,14 @@ podp_status validate(const podp_operators &o, int idx) {
     return fail(PODP_ERR_ARG, "object %d: alpha_lb must be finite and > 0", idx);
   const int r = o.r, ng = 6 + 2 * r;
   const size_t rr = (size_t)2 * r * r;
-  if (!all_finite(o.K, rr) || !all_finite(o.M, rr) || (o.K_R && !all_finite(o.K_R, rr)) ||
+  if (!all_finite(o.K, rr) || !all_finite(o.M, rr) || (o.K_R && !all_finite(o.K_R, rr)) || (o.M_I && !all_finite(o.M_I, rr)) ||
       !all_finite(o.b0, 6 * (size_t)r) || !all_finite(o.b1, 6 * (size_t)r) || !all_finite(o.N0, 9) ||
       !all_finite(o.S, 9) || !all_finite(o.H, 6 * (size_t)r) || !all_finite(o.G, (size_t)2 * ng * ng))
     return fail(PODP_ERR_NONFINITE, "object %d: non-finite operator entry", idx);
   if (!is_hermitian(o.K, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: K is not Hermitian", idx);
   if (!is_hermitian(o.M, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: M is not Hermitian", idx);
   if (o.K_R && !is_hermitian(o.K_R, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: K_R is not Hermitian", idx);
+  if (o.M_I && !is_hermitian(o.M_I, r)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: M_I is not Hermitian", idx);
   if (!is_hermitian(o.G, ng)) return fail(PODP_ERR_NOT_HERMITIAN, "object %d: G is not Hermitian", idx);
   if (!is_symmetric3(o.S) || !is_symmetric3(o.N0)) return fail(PODP_ERR_ARG, "object %d: S / N0 not symmetric", idx);
   return PODP_OK;
@@ -143,6 +144,7 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
         dst[L.K + e] = in ? C(o.K, r, i, j, c) : (i == j && c == 0 ? 1.0 : 0.0);  // K_pad = diag(K, I)
         dst[L.M + e] = in ? C(o.M, r, i, j, c) : 0.0;
         dst[L.KR + e] = in ? C(o.K_R ? o.K_R : o.K, r, i, j, c) : 0.0;
+        dst[L.MI + e] = in ? C(o.M_I ? o.M_I : o.M, r, i, j, c) : 0.0;
         dst[L.Gkk + e] = in ? C(o.G, ng, 6 + i, 6 + j, c) : 0.0;
         dst[L.Gmm + e] = in ? C(o.G, ng, 6 + r + i, 6 + r + j, c) : 0.0;
       }
@@ -211,6 +213,7 @@ Layout make_layout(int R) {
   L.K = take(sq);
   L.M = take(sq);
   L.KR = take(sq);
+  L.MI = take(sq);
   L.Gkk = take(sq);
   L.J = take(sq);
   L.Gmm = take(sq);

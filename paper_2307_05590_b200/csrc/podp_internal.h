@@ -12,7 +12,7 @@ namespace podp {
 // K_pad = diag(K, I), everything else zero-padded; SURVEY 7 "Padding r ... is exact").
 struct Layout {
   int R;          // padded r
-  int64_t K, M, KR, Gkk, J, Gmm;  // R x R complex
+  int64_t K, M, KR, MI, Gkk, J, Gmm;  // R x R complex (MI: mass in I; = M unless per-direction, N1)
   int64_t b0, b1, H;              // 3 x R complex (direction-major: b0[c*R + i] = b0_user[i][c])
   int64_t GbK, GbM;               // 6 x R complex (row a = b-slot a)
   int64_t Gbb;                    // 6 x 6 complex

@@ -39,7 +39,7 @@ class PodpError(RuntimeError):
 class podp_operators(ctypes.Structure):
     _fields_ = [("r", ctypes.c_int32), ("nu", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("alpha_lb", ctypes.c_double)] + [
-        (n, ctypes.POINTER(ctypes.c_double)) for n in ("K", "M", "K_R", "b0", "b1", "N0", "S", "H", "G")]
+        (n, ctypes.POINTER(ctypes.c_double)) for n in ("K", "M", "K_R", "b0", "b1", "N0", "S", "H", "G", "M_I")]
 
 
 _lib = None
@@ -165,7 +165,7 @@ def _f64(x, shape) -> np.ndarray:
 
 
 def _marshal(o, keep: list) -> podp_operators:
-    """Duck-typed operator object (attributes K, M, K_R?, b0, b1, N0, S, H, G, nu, alpha, alpha_lb)."""
+    """Duck-typed operator object (attributes K, M, K_R?, M_I?, b0, b1, N0, S, H, G, nu, alpha, alpha_lb)."""
     r = int(np.asarray(o.K).shape[0])
     st = podp_operators()
     st.r = r
@@ -173,9 +173,10 @@ def _marshal(o, keep: list) -> podp_operators:
     arrays = dict(K=_c128(o.K, (r, r)), M=_c128(o.M, (r, r)), b0=_c128(o.b0, (r, 3)), b1=_c128(o.b1, (r, 3)),
                   N0=_f64(o.N0, (3, 3)), S=_f64(o.S, (3, 3)), H=_c128(o.H, (3, r)),
                   G=_c128(o.G, (6 + 2 * r, 6 + 2 * r)))
-    kr = getattr(o, "K_R", None)
-    if kr is not None:
-        arrays["K_R"] = _c128(kr, (r, r))
+    for name in ("K_R", "M_I"):
+        x = getattr(o, name, None)
+        if x is not None:
+            arrays[name] = _c128(x, (r, r))
     for k, a in arrays.items():
         keep.append(a)
         setattr(st, k, _dptr(a))

@@ -101,3 +101,23 @@ def test_N2_gpu_driver_matches_oracle(torch_cuda, fom, vol, run4):
     T1, I = out["T1"][0].cpu().numpy(), out["I"][0].cpu().numpy()
     assert np.max(np.abs(T1 - oT1)) <= 1e-9 * np.max(np.abs(oT1))
     assert np.max(np.abs(I - oI)) <= 1e-9 * np.max(np.abs(oI))
+
+
+def test_N2_oracle_per_direction_runs(fom, vol):
+    # N1 inside Algorithm 1: per-direction TSVDs (lines 6/19 for i = 1, 2, 3); same snapshot bookkeeping
+    _o, _x, h = oadapt.run_adaptive(fom, OMEGA, tol_delta=1e-12, max_k=3, vol=vol, per_direction=True)
+    assert [x["N"] for x in h] == [13, 15, 17] and all(len(x["m"]) == 3 for x in h)
+    assert h[-1]["Lambda"] < h[0]["Lambda"]
+
+
+@pytest.mark.gpu
+def test_N2_gpu_driver_per_direction_matches_oracle(torch_cuda, fom, vol):
+    from paper_2307_05590_b200 import adapt
+    _ops, out, h = adapt.run_adaptive(fom, OMEGA, tol_delta=1e-12, max_k=3, vol=vol, per_direction=True)
+    _o, (oT1, oI, _oD), oh = oadapt.run_adaptive(fom, OMEGA, tol_delta=1e-12, max_k=3, vol=vol, per_direction=True)
+    for a, b in zip(h, oh):
+        assert a["m"] == b["m"] and a["snap"] == b["snap"] and a["new"] == b["new"]
+        assert abs(a["Lambda"] - b["Lambda"]) <= 1e-2 * b["Lambda"]
+    T1, I = out["T1"][0].cpu().numpy(), out["I"][0].cpu().numpy()
+    assert np.max(np.abs(T1 - oT1)) <= 1e-9 * np.max(np.abs(oT1))
+    assert np.max(np.abs(I - oI)) <= 1e-9 * np.max(np.abs(oI))
