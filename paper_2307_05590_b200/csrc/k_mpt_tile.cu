@@ -253,10 +253,11 @@ static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s) {
 
 cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s) {
   switch (a.L.R) {
-    case 24: return launch_mpt_tile_t<24>(a, s);
-    case 32: return launch_mpt_tile_t<32>(a, s);
-    case 48: return launch_mpt_tile_t<48>(a, s);
-    case 96: return launch_mpt_tile_t<96>(a, s);
+#define PODP_MT(R) \
+    case R: return launch_mpt_tile_t<R>(a, s);
+    PODP_MT(8) PODP_MT(16) PODP_MT(24) PODP_MT(32) PODP_MT(40) PODP_MT(48) PODP_MT(56) PODP_MT(64)
+    PODP_MT(72) PODP_MT(80) PODP_MT(88) PODP_MT(96) PODP_MT(104) PODP_MT(112) PODP_MT(120) PODP_MT(128)
+#undef PODP_MT
     default: return cudaErrorNotSupported;
   }
 }

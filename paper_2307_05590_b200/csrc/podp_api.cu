@@ -175,15 +175,25 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   double *sc = dst + L.scal;
   sc[podp::SC_NU] = o.nu;
   sc[podp::SC_PENCIL_OK] = 0.0;
-  if (R == r) {
+  {
+    // pencil precompute on the true r; the padding (K_pad = diag(K, I), M_pad = 0) extends it exactly with
+    // Z_pad = diag(Z, I), lambda_pad = 0, c_pad = 0
     std::vector<double> Z, lam, c0, c1;
     if (podp::pencil_precompute(r, o.K, o.M, o.b0, o.b1, Z, lam, c0, c1)) {
-      for (size_t e = 0; e < Z.size(); ++e) dst[L.Z + e] = Z[e];
+      for (int i = 0; i < R; ++i)
+        for (int j = 0; j < R; ++j) {
+          const size_t e = 2 * ((size_t)i * R + j);
+          const bool in = i < r && j < r;
+          dst[L.Z + e] = in ? Z[2 * ((size_t)i * r + j)] : (i == j ? 1.0 : 0.0);
+          dst[L.Z + e + 1] = in ? Z[2 * ((size_t)i * r + j) + 1] : 0.0;
+        }
       for (int e = 0; e < r; ++e) dst[L.lam + e] = lam[e];
-      for (size_t e = 0; e < c0.size(); ++e) {
-        dst[L.c0 + e] = c0[e];
-        dst[L.c1 + e] = c1[e];
-      }
+      for (int c3 = 0; c3 < 3; ++c3)
+        for (int k = 0; k < r; ++k)
+          for (int c = 0; c < 2; ++c) {
+            dst[L.c0 + 2 * ((size_t)c3 * R + k) + c] = c0[2 * ((size_t)c3 * r + k) + c];
+            dst[L.c1 + 2 * ((size_t)c3 * R + k) + c] = c1[2 * ((size_t)c3 * r + k) + c];
+          }
       sc[podp::SC_PENCIL_OK] = 1.0;
     }
   }
@@ -195,7 +205,9 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   }
 }
 
-int choose_R(int r) { return r; }
+// Padded size: next multiple of 8 (the specialised kernels exist for R = 8, 16, ..., 128); the padding is exact
+// (K_pad = diag(K, I), every other operator zero-padded).
+int choose_R(int r) { return (r + 7) / 8 * 8; }
 
 }  // namespace
 
