@@ -416,14 +416,8 @@ cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s) {
     if (a.L.R == 48) return launch_lu_reg_t<48, 4, 4, false>(a, s);
     return cudaErrorNotSupported;
   }
-  const char *v = getenv("PODP_LU_VARIANT");
-  const int var = v ? atoi(v) : 0;
   switch (a.L.R) {
     case 48:
-      if (var == 1) return launch_lu_reg_t<48, 2, 4>(a, s);
-      if (var == 2) return launch_lu_reg_t<48, 4, 3>(a, s);
-      if (var == 3) return launch_lu_reg_t<48, 4, 1>(a, s);
-      if (var == 4) return launch_lu_reg_t<48, 4, 2>(a, s);
       return launch_lu_reg_t<48, 4, 4>(a, s);
     default: return cudaErrorNotSupported;
   }

@@ -481,6 +481,12 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
       fprintf(stderr, "omega %d: assembled %lld, LU done %lld, back-sub done %lld\n", q, tr[1] - tr[0], tr[2] - tr[0], tr[3] - tr[0]);
       for (int k = 0; k < 16 && tr[16 + 4 * k]; ++k)
         fprintf(stderr, "  panel %d: passed hand-off %lld  after lookahead %lld  after own tiles %lld\n", k, tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0]);
+      for (int k = 0; k < 12; ++k) {
+        if (!tr[100 + 8 * k]) continue;
+        fprintf(stderr, "  factor %d cols:", k);
+        for (int j = 0; j < 8; ++j) fprintf(stderr, " %lld", tr[100 + 8 * k + j] - tr[0]);
+        fprintf(stderr, " | loop end %lld | moves done %lld\n", tr[200 + k] - tr[0], tr[210 + k] - tr[0]);
+      }
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");
