@@ -14,6 +14,7 @@
 //     product is 4 real DMMAs; C fragments are read/written in shared memory, two tiles interleaved.
 //   * B rides along as columns R..R+2 (forward elimination); back substitution runs from the U rows in shared
 //     memory (one warp per right-hand side, solution column in registers).
+#include <cstdio>
 #include <cstdlib>
 
 #include "podp_common.cuh"
@@ -238,33 +239,25 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
     LB_TR(0);
-    // ---- a2: assemble [A | B | 0] (all W warps; K, M streamed from L2 with 12 loads in flight per lane) ----------
+    // ---- a2: assemble [A | B | 0] (all W warps).  K is copied into A by cp.async (16 B per element, all copies in
+    //      flight at once, no registers); M is streamed through registers in two batches meanwhile; each thread
+    //      then adds i s M to the K entries it copied itself (cp.async.wait_all orders its own copies). ------------
     {
       const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
       const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
       constexpr int PER = (R * R + NT - 1) / NT;
-      constexpr int BATCH = 12;
+      constexpr int HALF = (PER + 1) / 2;
       const int gl = w * 32 + lane;
-#pragma unroll 1
-      for (int e0 = 0; e0 < PER; e0 += BATCH) {
-        double2 kk[BATCH], mm[BATCH];
 #pragma unroll
-        for (int q = 0; q < BATCH; ++q) {
-          const int e = (e0 + q) * NT + gl;
-          if (e0 + q < PER && e < R * R) {
-            kk[q] = __ldg(gK + e);
-            mm[q] = __ldg(gM + e);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < BATCH; ++q) {
-          const int e = (e0 + q) * NT + gl;
-          if (e0 + q < PER && e < R * R) {
-            const int i = e / R, j = e - i * R;
-            A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk[q].x), fma(s, mm[q].x, kk[q].y));
-          }
+      for (int q = 0; q < PER; ++q) {
+        const int e = q * NT + gl;
+        if (e < R * R) {
+          const int i = e / R, j = e - i * R;
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(A + i * LDA + j);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gK + e) : "memory");
         }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
       const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
       const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
       for (int e = gl; e < 8 * R; e += NT) {
@@ -275,6 +268,25 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
           v = make_double2(fma(om, x1.x, x0.x), fma(om, x1.y, x0.y));
         }
         A[i * LDA + R + c] = v;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 mm[HALF];
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+          const int e = (h * HALF + q) * NT + gl;
+          if (h * HALF + q < PER && e < R * R) mm[q] = __ldg(gM + e);
+        }
+        if (h == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+          const int e = (h * HALF + q) * NT + gl;
+          if (h * HALF + q < PER && e < R * R) {
+            const int i = e / R, j = e - i * R;
+            const double2 kk = A[i * LDA + j];
+            A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk.x), fma(s, mm[q].x, kk.y));
+          }
+        }
       }
     }
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
@@ -402,7 +414,14 @@ static cudaError_t launch_lu_blk_t(const EvalArgs &a, cudaStream_t s) {
   int64_t blocks = (total + C::GROUPS - 1) / C::GROUPS;
   if (blocks > sms) blocks = sms;
   kern<<<(unsigned)blocks, C::THREADS, C::BYTES, s>>>(a);
-  return cudaGetLastError();
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess && getenv("PODP_LU_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "lu_blk<%d,%d>: threads %d bytes %zu regs %d maxThreads %d local %zu static_smem %zu\n", R, W,
+            C::THREADS, C::BYTES, fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes);
+  }
+  return le;
 }
 
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s) {

@@ -67,7 +67,7 @@ __global__ void probe(double2 *g, long long *out, int contend) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int kr = kb + j;
-      if (VAR == 0 && j > 0) {
+      if (VAR != 1 && j > 0) {
         key = 0u;
         cand = pn[0][j];
 #pragma unroll
@@ -76,8 +76,8 @@ __global__ void probe(double2 *g, long long *out, int contend) {
           if (pos[m] >= kr && pos[m] < R && kk > key) { key = kk; cand = pn[m][j]; }
         }
       }
-      const double2 rc_mine = crecip_fast(cand);
-      const unsigned best = __reduce_max_sync(FULL, key);
+      const double2 rc_mine = (VAR == 3 || VAR == 4) ? cand : crecip_fast(cand);
+      const unsigned best = (VAR == 2 || VAR == 4) ? (unsigned)(127 - kr) : __reduce_max_sync(FULL, key);
       const int p = 127 - (int)(best & 127u);
       bool mine[MS];
 #pragma unroll
@@ -141,15 +141,19 @@ __global__ void probe(double2 *g, long long *out, int contend) {
 
 int main() {
   double2 *g; long long *out;
-  cudaMalloc(&g, 48 * 57 * 16); cudaMallocManaged(&out, 64 * 8);
+  cudaMalloc(&g, 48 * 57 * 16); cudaMallocManaged(&out, 64 * 8); cudaMemset(out, 0, 64 * 8);
   static double2 h[48 * 57];
   for (int i = 0; i < 48 * 57; ++i) h[i] = make_double2(1.0 + (i * 7919 % 97) * 0.01, (i * 104729 % 89) * 0.01);
   for (int i = 0; i < 48; ++i) h[i * 57 + (i % 8)] = make_double2(100.0 + i, 0.0);
   for (int contend = 0; contend < 3; ++contend) {
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < 5; ++v) {
+      if (contend && v > 1) continue;
       cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
       if (v == 0) probe<0><<<1, 160>>>(g, out, contend);
       if (v == 1) probe<1><<<1, 160>>>(g, out, contend);
+      if (v == 2) probe<2><<<1, 160>>>(g, out, contend);
+      if (v == 3) probe<3><<<1, 160>>>(g, out, contend);
+      if (v == 4) probe<4><<<1, 160>>>(g, out, contend);
       cudaError_t e = cudaDeviceSynchronize();
       printf("{\"var\":%d,\"contend\":%d,\"clk_per_panel\":%lld,\"clk_per_column\":%lld,\"err\":\"%s\"}\n", v, contend,
              out[v * 3 + contend], out[v * 3 + contend] / 8, cudaGetErrorString(e));
