@@ -33,7 +33,10 @@ struct Cfg {
 
 }  // namespace mpttile
 
-template <int R>
+// DIAG (N3 pencil coordinates with K_R = K and M_I = M): Z^H K Z = I and Z^H M Z = Lambda, so the K_R and M_I
+// quadratic forms are diagonal -- Re(y_i^H y_j) and Re(y_i^H Lambda y_j) -- and are accumulated in the slice pass;
+// only Q~ = Z^H Q Z stays dense.
+template <int R, bool DIAG>
 __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalArgs a) {
   using C = mpttile::Cfg<R>;
   constexpr int NBL = C::NBL, RB = C::RB, NBLK = C::NBLK, LD = C::LD, SL = C::SL, TILE = C::TILE, FPW = C::FPW;
@@ -72,6 +75,24 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
     double qK[6], qM[6], qQ[6], lp[9], hp[9];
 #pragma unroll
     for (int e = 0; e < 6; ++e) qK[e] = qM[e] = qQ[e] = 0.0;
+    if constexpr (DIAG) {
+      const double *lam = op + a.L.lam;
+#pragma unroll
+      for (int tt = 0; tt < NBL; ++tt) {
+        const int b = sl + SL * tt;
+        if (b < R) {
+          const double lb = lam[b];
+#pragma unroll
+          for (int e = 0; e < 6; ++e) {
+            const int i = e < 3 ? e : (e < 5 ? 0 : 1);
+            const int j = e < 3 ? e : (e == 3 ? 1 : 2);
+            const double re = fma(p[tt][i].x, p[tt][j].x, p[tt][i].y * p[tt][j].y);
+            qK[e] += re;
+            qM[e] = fma(lb, re, qM[e]);
+          }
+        }
+      }
+    }
     // linear terms over my slice: Re(l_i[b] p_j[b]), Re(h_i[b] p_j[b])
     {
       const double2 *GbK = reinterpret_cast<const double2 *>(op + a.L.GbK);
@@ -117,8 +138,10 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
         for (int e = threadIdx.x; e < n; e += blockDim.x) {
           const int row = e / R, col = e - row * R;
           const int src = (a0 + row) * R + col, dst = row * LD + col;
-          sKR[dst] = gKR[src];
-          sM[dst] = gM[src];
+          if constexpr (!DIAG) {
+            sKR[dst] = gKR[src];
+            sM[dst] = gM[src];
+          }
           sGk[dst] = gGk[src];
           sJ[dst] = gJ[src];
           sGm[dst] = gGm[src];
@@ -147,23 +170,28 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
         for (int tt = 0; tt < NBL; ++tt) {
           const int b = sl + SL * tt;
           if ((R % SL) == 0 || b < R) {
-            const double2 kr = oKR[row + b], mm = oM[row + b];
             const double2 gk = oGk[row + b], jj = oJ[row + b], gm = oGm[row + b];
             const double2 q = make_double2(fma(s, fma(s, gm.x, jj.x), gk.x), fma(s, fma(s, gm.y, jj.y), gk.y));
+            if constexpr (!DIAG) {
+              const double2 kr = oKR[row + b], mm = oM[row + b];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              yK[c] = cfma(kr, p[tt][c], yK[c]);
-              yM[c] = cfma(mm, p[tt][c], yM[c]);
-              yQ[c] = cfma(q, p[tt][c], yQ[c]);
+              for (int c = 0; c < 3; ++c) {
+                yK[c] = cfma(kr, p[tt][c], yK[c]);
+                yM[c] = cfma(mm, p[tt][c], yM[c]);
+              }
             }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) yQ[c] = cfma(q, p[tt][c], yQ[c]);
           }
         }
 #pragma unroll
         for (int e = 0; e < 6; ++e) {
           const int i = e < 3 ? e : (e < 5 ? 0 : 1);
           const int j = e < 3 ? e : (e == 3 ? 1 : 2);
-          qK[e] = fma(pa[i].x, yK[j].x, fma(pa[i].y, yK[j].y, qK[e]));
-          qM[e] = fma(pa[i].x, yM[j].x, fma(pa[i].y, yM[j].y, qM[e]));
+          if constexpr (!DIAG) {
+            qK[e] = fma(pa[i].x, yK[j].x, fma(pa[i].y, yK[j].y, qK[e]));
+            qM[e] = fma(pa[i].x, yM[j].x, fma(pa[i].y, yM[j].y, qM[e]));
+          }
           qQ[e] = fma(pa[i].x, yQ[j].x, fma(pa[i].y, yQ[j].y, qQ[e]));
         }
       }
@@ -236,9 +264,9 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
 }
 
 template <int R>
-static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s) {
+static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s, bool diag) {
   using C = mpttile::Cfg<R>;
-  auto kern = mpt_tile_kernel<R>;
+  auto kern = diag ? mpt_tile_kernel<R, true> : mpt_tile_kernel<R, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -251,10 +279,10 @@ static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s) {
+cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag) {
   switch (a.L.R) {
 #define PODP_MT(R) \
-    case R: return launch_mpt_tile_t<R>(a, s);
+    case R: return launch_mpt_tile_t<R>(a, s, diag);
     PODP_MT(8) PODP_MT(16) PODP_MT(24) PODP_MT(32) PODP_MT(40) PODP_MT(48) PODP_MT(56) PODP_MT(64)
     PODP_MT(72) PODP_MT(80) PODP_MT(88) PODP_MT(96) PODP_MT(104) PODP_MT(112) PODP_MT(120) PODP_MT(128)
 #undef PODP_MT

@@ -106,3 +106,49 @@ cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s) {
 }
 
 }  // namespace podp
+
+namespace podp {
+
+// N3 fast path: y(omega) = diag(1/(1 + i s lambda)) (c0 + omega c1), s = omega nu -- O(r) per frequency; the
+// MPT/certificate kernel then runs on y with the operators in pencil coordinates (podp_api.cu pencil_transform).
+__global__ void __launch_bounds__(256) pencil_y_kernel(EvalArgs a) {
+  const int R = a.L.R;
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  const int64_t n = total * R;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = g / R;
+    const int b = (int)(g - t * R);
+    const int obj = (int)(t / a.F);
+    const int64_t f = t - (int64_t)obj * a.F;
+    const double *op = a.ops + (size_t)obj * a.L.stride;
+    const double w = a.omega[f];
+    const bool ok = isfinite(w);
+    const double sl = w * op[a.L.scal + SC_NU] * op[a.L.lam + b];
+    const double den = 1.0 / fma(sl, sl, 1.0);
+    const double2 d = make_double2(den, -sl * den);
+    const double2 *c0 = reinterpret_cast<const double2 *>(op + a.L.c0);
+    const double2 *c1 = reinterpret_cast<const double2 *>(op + a.L.c1);
+    double2 *Pw = a.Pws + (size_t)t * 3 * R;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double2 x0 = c0[c * R + b], x1 = c1[c * R + b];
+      const double2 y = cmul(d, make_double2(fma(w, x1.x, x0.x), fma(w, x1.y, x0.y)));
+      Pw[c * R + b] = ok ? y : make_double2(nanv, nanv);
+    }
+    if (a.info && b == 0) a.info[t] = ok ? 0 : -1;
+  }
+}
+
+cudaError_t launch_pencil_y(const EvalArgs &a, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n = (int64_t)a.n_obj * a.F * a.L.R;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  pencil_y_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace podp

@@ -1,6 +1,7 @@
 // libpodp C ABI (include/podp.h): validation, packing (row a1 of SURVEY 8(a)), launch orchestration.
 // Host-side only; kernels live in k_solve.cu (a2-a3), k_mpt.cu (a4-a6) and k_select.cu (a7).
 #include <cmath>
+#include <complex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -12,6 +13,7 @@
 
 struct podp_ctx {
   bool pencil_ok;      // pencil precompute available (K positive definite for every object)
+  bool pencil_diag;    // every object has K_R = K and M_I = M: Z^H K_R Z = I, Z^H M_I Z = Lambda exactly
   int device;
   int r;
   int n_obj;
@@ -132,6 +134,44 @@ podp_status validate(const podp_operators &o, int idx) {
   return PODP_OK;
 }
 
+// N3: operators in pencil coordinates (P = Z y).  Quadratic forms p_i^H X p_j = y_i^H (Z^H X Z) y_j and linear
+// forms h p = (h Z) y, so the MPT/certificate kernel runs unchanged on y with X~ = Z^H X Z, H~ = H Z,
+// G~_bK = G_bK Z, G~_bM = G_bM Z (all already padded to R; Z_pad = diag(Z, I)).
+void pencil_transform(const podp::Layout &L, double *dst) {
+  using cd = std::complex<double>;
+  const int R = L.R;
+  auto at = [&](int64_t base, int ld, int i, int j) { return cd(dst[base + 2 * ((size_t)i * ld + j)], dst[base + 2 * ((size_t)i * ld + j) + 1]); };
+  std::vector<cd> Z((size_t)R * R), T((size_t)R * R);
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) Z[(size_t)i * R + j] = at(L.Z, R, i, j);
+  const int64_t src[5] = {L.KR, L.MI, L.Gkk, L.J, L.Gmm}, dstb[5] = {L.PKR, L.PMI, L.PGkk, L.PJ, L.PGmm};
+  for (int q = 0; q < 5; ++q) {
+    for (int i = 0; i < R; ++i)  // T = X Z
+      for (int j = 0; j < R; ++j) {
+        cd acc = 0.0;
+        for (int k = 0; k < R; ++k) acc += at(src[q], R, i, k) * Z[(size_t)k * R + j];
+        T[(size_t)i * R + j] = acc;
+      }
+    for (int i = 0; i < R; ++i)  // Z^H T
+      for (int j = 0; j < R; ++j) {
+        cd acc = 0.0;
+        for (int k = 0; k < R; ++k) acc += std::conj(Z[(size_t)k * R + i]) * T[(size_t)k * R + j];
+        dst[dstb[q] + 2 * ((size_t)i * R + j)] = acc.real();
+        dst[dstb[q] + 2 * ((size_t)i * R + j) + 1] = acc.imag();
+      }
+  }
+  const int64_t vs[3] = {L.H, L.GbK, L.GbM}, vd[3] = {L.PH, L.PGbK, L.PGbM};
+  const int rows[3] = {3, 6, 6};
+  for (int q = 0; q < 3; ++q)
+    for (int a = 0; a < rows[q]; ++a)
+      for (int j = 0; j < R; ++j) {
+        cd acc = 0.0;
+        for (int k = 0; k < R; ++k) acc += at(vs[q], R, a, k) * Z[(size_t)k * R + j];
+        dst[vd[q] + 2 * ((size_t)a * R + j)] = acc.real();
+        dst[vd[q] + 2 * ((size_t)a * R + j) + 1] = acc.imag();
+      }
+}
+
 // Pack one object into dst (L.stride doubles, zero-initialised by the caller).
 void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   const int r = o.r, R = L.R, ng = 6 + 2 * r;
@@ -195,6 +235,8 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
             dst[L.c1 + 2 * ((size_t)c3 * R + k) + c] = c1[2 * ((size_t)c3 * r + k) + c];
           }
       sc[podp::SC_PENCIL_OK] = 1.0;
+      pencil_transform(L, dst);
+      sc[podp::SC_PENCIL_DIAG] = (o.K_R == nullptr && o.M_I == nullptr) ? 1.0 : 0.0;
     }
   }
   sc[podp::SC_ALPHA] = o.alpha;
@@ -240,6 +282,14 @@ Layout make_layout(int R) {
   L.lam = take(R);
   L.c0 = take(vec3);
   L.c1 = take(vec3);
+  L.PKR = take(sq);
+  L.PMI = take(sq);
+  L.PGkk = take(sq);
+  L.PJ = take(sq);
+  L.PGmm = take(sq);
+  L.PH = take(vec3);
+  L.PGbK = take(vec6);
+  L.PGbM = take(vec6);
   L.stride = off;
   return L;
 }
@@ -306,6 +356,8 @@ podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int devi
   podp_ctx *c = new podp_ctx;
   c->pencil_ok = true;
   for (int k = 0; k < n_obj; ++k) c->pencil_ok &= host[(size_t)L.stride * k + L.scal + podp::SC_PENCIL_OK] == 1.0;
+  c->pencil_diag = c->pencil_ok;
+  for (int k = 0; k < n_obj; ++k) c->pencil_diag &= host[(size_t)L.stride * k + L.scal + podp::SC_PENCIL_DIAG] == 1.0;
   c->pool = pool;
   c->device = device;
   c->r = r;
@@ -439,10 +491,24 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   cudaError_t e = cudaMallocFromPoolAsync((void **)&a.Pws, ws, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
   int nl = 0;
+  // N3 without the debug P output: solve for y only and run the MPT/certificate kernel in pencil coordinates
+  const bool pencil_y = (flags & PODP_FLAG_PENCIL) && !(flags & PODP_FLAG_OUT_P) && !getenv("PODP_PENCIL_P");
+  podp::EvalArgs am = a;
+  if (pencil_y) {
+    am.L.KR = c->L.PKR;
+    am.L.MI = c->L.PMI;
+    am.L.Gkk = c->L.PGkk;
+    am.L.J = c->L.PJ;
+    am.L.Gmm = c->L.PGmm;
+    am.L.H = c->L.PH;
+    am.L.GbK = c->L.PGbK;
+    am.L.GbM = c->L.PGbM;
+  }
   {
     ProfScope ps("solve", s);
     const char *lv = getenv("PODP_LU_IMPL");  // dev switch: "reg" = register-resident kernel, default blocked
-    if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
+    if ((flags & PODP_FLAG_PENCIL) && pencil_y) e = podp::launch_pencil_y(a, s);
+    else if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
     else if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
     else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
     else if (lv && lv[0] == 'p') e = podp::launch_lu_pw(a, s);
@@ -463,12 +529,13 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   }
   if (e == cudaSuccess) {
     ProfScope ps("mpt", s);
-    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported : podp::launch_mpt_tile(a, s);
+    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported
+                                              : podp::launch_mpt_tile(am, s, pencil_y && c->pencil_diag);
     if (e == cudaSuccess) {
       ++nl;
     } else if (e == cudaErrorNotSupported) {
       cudaGetLastError();
-      e = podp::launch_mpt(a, s, &nl);
+      e = podp::launch_mpt(am, s, &nl);
     }
   }
   cudaFreeAsync(a.Pws, s);

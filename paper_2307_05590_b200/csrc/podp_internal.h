@@ -18,10 +18,13 @@ struct Layout {
   int64_t Gbb;                    // 6 x 6 complex
   int64_t scal;                   // SCAL_N doubles (see below)
   int64_t Z, lam, c0, c1;         // pencil precompute (N3): Z (R x R complex), lambda (R), c0, c1 (3 x R complex)
+  // N3 operators in the pencil coordinates y (P = Z y): X~ = Z^H X Z for K_R, M_I, G_KK, J, G_MM; H~ = H Z;
+  // G~_bK = G_bK Z, G~_bM = G_bM Z.  The MPT/certificate kernel runs on y with these unchanged.
+  int64_t PKR, PMI, PGkk, PJ, PGmm, PH, PGbK, PGbM;
   int64_t stride;                 // doubles per object (multiple of 32)
 };
 
-enum { SC_NU = 0, SC_ALPHA = 1, SC_ALPHA_LB = 2, SC_PENCIL_OK = 3, SC_S = 4, SC_N0 = 13, SCAL_N = 32 };
+enum { SC_NU = 0, SC_ALPHA = 1, SC_ALPHA_LB = 2, SC_PENCIL_OK = 3, SC_S = 4, SC_N0 = 13, SC_PENCIL_DIAG = 22, SCAL_N = 32 };
 
 Layout make_layout(int R);
 
@@ -45,10 +48,11 @@ struct EvalArgs {
 #define PODP_INTERNAL_FORCE_GENERIC (1 << 16)
 
 cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
-cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s);  // cudaErrorNotSupported if no instantiation
+cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag = false);  // NotSupported if no instantiation
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_lu_pw(const EvalArgs &a, cudaStream_t s);     // cudaErrorNotSupported if no instantiation
 cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
+cudaError_t launch_pencil_y(const EvalArgs &a, cudaStream_t s);  // N3: y = (I + i s Lambda)^{-1}(c0 + omega c1) only
 cudaError_t launch_invariants(const double *T1, const double *I, int64_t n, double *eigR, double *eigI, cudaStream_t s);
 cudaError_t launch_coil_voltage(const double *T1, const double *I, int64_t n, const double *hex_d, const double *hms_d,
                                 int n_coil, double *V, cudaStream_t s);

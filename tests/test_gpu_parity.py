@@ -286,6 +286,11 @@ def test_pencil_solver_parity(torch_cuda, r, F):
     for f in range(0, F, max(1, F // 13)):
         Po = solve_reduced(ops.K, ops.M, ops.b0, ops.b1, ops.nu, float(omega[f]))
         assert np.linalg.norm(res["P"][0, f].T - Po) / np.linalg.norm(Po) <= 1e-10
+    # without the debug P output the MPT/certificate kernel runs in pencil coordinates (y, Z^H X Z; diagonal
+    # K_R and M_I forms since K_R = K and M_I = M here)
+    res_y = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_PENCIL)
+    assert (res_y["info"] == 0).all()
+    check_parity(ops, omega, res_y)
 
 
 def test_pencil_batch_and_unsupported(torch_cuda):
