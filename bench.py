@@ -282,7 +282,9 @@ def main():
         pprof = pb.profile_read(reset=True)
         pb.profile_enable(False)
         r = R_HEAD
-        exec_flops = 8.0 * 3 * r * r + 3 * 8 * r + falg_mpt(r)  # Z y (3 r^2 cmad) + scaling + MPT/certificate
+        # executed per frequency on the y path: y = D (c0 + omega c1) (~30 r), Q~ = G~kk + s J~ + s^2 G~mm (8 r^2),
+        # Q~ y for 3 columns (24 r^2), diagonal K_R / M_I forms + linear terms + epilogue (~190 r)
+        exec_flops = 32.0 * r * r + 220.0 * r
         pen_val = F * args.steps / (pen_ms / 1e3)
         variants["pencil_N3"] = {
             "value": pen_val, "unit": UNIT, "ms_per_eval": pen_ms / args.steps,
@@ -290,7 +292,8 @@ def main():
             "executed_tflops": exec_flops * pen_val / 1e12,
             "frac_of_fp64_peak_executed": exec_flops * pen_val / 1e12 / FP64_PEAK_TFLOPS,
             "kernel_ms_per_eval": {k: v[0] / max(v[1], 1) for k, v in pprof.items()},
-            "note": "exact reformulation (K = L L^H, L^-1 M L^-H = V Lambda V^H); NEXT row N3, not the LU headline"}
+            "note": "exact reformulation (K = L L^H, L^-1 M L^-H = V Lambda V^H, y = (I + i s Lambda)^-1 Z^H B, MPT and "
+                    "certificate in pencil coordinates); NEXT row N3, not the LU headline"}
     except Exception as exc:  # pragma: no cover
         variants["pencil_N3"] = {"error": str(exc)[:200]}
     # NEXT row N2: one Algorithm-1 run (off-line cuSOLVER/cuBLAS + on-line libpodp certification on a 1e5 grid)
