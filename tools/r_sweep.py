@@ -7,7 +7,7 @@ import numpy as np
 import torch
 
 import podp_inputs as g
-from paper_2307_05590_b200 import FLAG_PENCIL, Evaluator
+from paper_2307_05590_b200 import FLAG_PENCIL, Evaluator, profile_enable, profile_read
 
 
 def ops_for(r):
@@ -28,10 +28,13 @@ def main():
         ev = Evaluator(ops_for(r))
         out = ev.alloc_outputs(F)
         res = []
+        split = []
         for flags in (0, FLAG_PENCIL):
             for _ in range(2):
                 ev.eval(w, out=out, flags=flags)
             torch.cuda.synchronize()
+            profile_enable(True)
+            profile_read(reset=True)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(3):
@@ -39,7 +42,10 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             res.append(e0.elapsed_time(e1) / 3)
-        print(f"r={r:3d} lu_ms={res[0]:8.3f} pencil_ms={res[1]:8.3f}", flush=True)
+            pr = profile_read(reset=True)
+            profile_enable(False)
+            split.append("/".join(f"{k}={v[0] / max(v[1], 1):.3f}" for k, v in pr.items()))
+        print(f"r={r:3d} lu_ms={res[0]:8.3f} pencil_ms={res[1]:8.3f}   [{split[0]}] [{split[1]}]", flush=True)
         ev.close()
 
 
