@@ -427,14 +427,15 @@ static cudaError_t launch_lu_blk_t(const EvalArgs &a, cudaStream_t s) {
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
   const char *v = getenv("PODP_LU_W");
-  // measured on B200 (tools/quick_time.py): one warp per frequency is best for r <= 32, two for r = 40..56,
-  // four for r >= 64 (shared memory then holds a single frequency per SM)
-  const int wv = v ? atoi(v) : (a.L.R >= 64 ? 4 : (a.L.R >= 40 ? 2 : 1));
+  // measured on B200 (tools/r_sweep.py): one warp per frequency is best for r <= 32, two for r = 40..56, four for
+  // r = 64..72, eight for r >= 80 (shared memory then holds a single frequency per SM)
+  const int wv = v ? atoi(v) : (a.L.R >= 80 ? 8 : (a.L.R >= 64 ? 4 : (a.L.R >= 40 ? 2 : 1)));
   switch (a.L.R) {
 #define PODP_CASE(RR)                                 \
   case RR:                                            \
     if (wv == 1) return launch_lu_blk_t<RR, 1>(a, s); \
     if (wv == 2) return launch_lu_blk_t<RR, 2>(a, s); \
+    if (wv == 8 && RR >= 64) return launch_lu_blk_t<(RR >= 64 ? RR : 64), 8>(a, s); \
     return launch_lu_blk_t<RR, 4>(a, s);
     PODP_CASE(8)
     PODP_CASE(16)

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpodp.so")
+LIB_PATH = os.path.join(_PKG, os.environ.get("PODP_LIB_NAME", "libpodp.so"))  # env: dev A/B builds only
 
 PODP_OK = 0
 FLAG_DEFAULT = 0

@@ -31,6 +31,12 @@ __global__ void probe(double2 *g, long long *out, int contend) {
       if (contend == 1) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) dmma(c[q][0], c[q][1], av, bv);
+      } else if (contend == 3) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dmma(c[0][0], c[0][1], av, bv);  // one dependent chain
+      } else if (contend == 4) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dmma(c[q & 1][0], c[q & 1][1], av, bv);  // two chains
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -135,7 +141,7 @@ __global__ void probe(double2 *g, long long *out, int contend) {
     __syncwarp();
   }
   long long t1 = clock64();
-  if (lane == 0) { out[VAR * 3 + contend] = (t1 - t0) / 16; done = 1; }
+  if (lane == 0) { out[VAR * 5 + contend] = (t1 - t0) / 16; done = 1; }
   for (int e = lane; e < R * LDA; e += 32) g[e] = A[e];
 }
 
@@ -145,7 +151,7 @@ int main() {
   static double2 h[48 * 57];
   for (int i = 0; i < 48 * 57; ++i) h[i] = make_double2(1.0 + (i * 7919 % 97) * 0.01, (i * 104729 % 89) * 0.01);
   for (int i = 0; i < 48; ++i) h[i * 57 + (i % 8)] = make_double2(100.0 + i, 0.0);
-  for (int contend = 0; contend < 3; ++contend) {
+  for (int contend = 0; contend < 5; ++contend) {
     for (int v = 0; v < 5; ++v) {
       if (contend && v > 1) continue;
       cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
@@ -156,7 +162,7 @@ int main() {
       if (v == 4) probe<4><<<1, 160>>>(g, out, contend);
       cudaError_t e = cudaDeviceSynchronize();
       printf("{\"var\":%d,\"contend\":%d,\"clk_per_panel\":%lld,\"clk_per_column\":%lld,\"err\":\"%s\"}\n", v, contend,
-             out[v * 3 + contend], out[v * 3 + contend] / 8, cudaGetErrorString(e));
+             out[v * 5 + contend], out[v * 5 + contend] / 8, cudaGetErrorString(e));
     }
   }
   return 0;
