@@ -244,6 +244,24 @@ def test_eval_host_matches_device(torch_cuda):
     ev.close()
 
 
+def test_eval_host_batch_nan(torch_cuda):
+    """Host entry with several objects and a failed frequency: results must equal the device entry bit for bit."""
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    ops = [g.make_operators(24, seed=k) for k in range(2)]
+    omega = g.omega_grid(90_001)
+    omega[777] = np.nan                       # a failed frequency inside a chunk
+    ev = Evaluator(ops)
+    h = ev.eval_host(omega, flags=FLAG_OUT_R)
+    d = ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_OUT_R)
+    torch.cuda.synchronize()
+    for k in ("T1", "I", "Delta"):
+        assert np.array_equal(h[k], d[k].cpu().numpy(), equal_nan=True), k
+    assert np.array_equal(h["info"], d["info"].cpu().numpy())
+    assert (h["info"][:, 777] == -1).all() and (np.delete(h["info"], 777, axis=1) == 0).all()
+    ev.close()
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_full_size_configs_sampled(torch_cuda, cfg):
