@@ -39,17 +39,27 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    # objects are rebuilt when their source, any shared header or the flags changed (stamp file per object)
+    hdr_t = max(os.path.getmtime(d) for d in deps() if not d.endswith(".cu"))
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-dc" if False else "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
-        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
+        stamp = obj + ".cmd"
+        fresh = (not force and os.path.exists(obj) and os.path.exists(stamp)
+                 and open(stamp).read() == " ".join(cmd)
+                 and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t))
+        if fresh:
+            continue
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for cmd, p in procs:
         out, _ = p.communicate()
         if p.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out)
+        with open(cmd[cmd.index("-o") + 1] + ".cmd", "w") as f:
+            f.write(" ".join(cmd))
         if verbose and out:
             sys.stdout.write(out)
     tmp = LIB + ".tmp"

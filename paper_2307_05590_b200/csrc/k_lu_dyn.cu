@@ -1,0 +1,682 @@
+// K2 default path: batched shifted complex LU with partial pivoting + 3-RHS solve, dynamically scheduled (rows a2-a3).
+//   A(omega) = K + i omega nu M,  B(omega) = b0 + omega b1,  P = A^{-1} B            (eqn:ReducedA)
+//   "the cost of solving (eqn:ReducedA) is at most O(M^3)": this kernel is that O(r^3) step.
+//
+// One group of W warps owns one frequency at a time; [A | B] (R x (R+3) complex, zero-padded to R x (R+8)) lives in
+// the group's slice of shared memory.  The columns are cut into 8-wide tile-columns; tile-column c belongs to warp
+// c mod W.  Two kinds of task exist:
+//   F(k)     factor panel k (tile-column k, rows 8k..R-1) with partial pivoting -- in registers, one warp, lane = row;
+//            the pivot search is one redux.sync over an integer magnitude key, the pivot row is broadcast by
+//            shuffles (no shared-memory round trip on the per-column chain), 1/pivot is MUFU.RCP64H + 2 Newton steps.
+//            Rows never move inside the panel; the panel is written back at the rows' final positions together with
+//            the step's permutation (orig[] / dst[]), then published (release store of a counter in shared memory).
+//   U(k, c)  apply panel k to tile-column c: permute the column in one pass (the 8 pivot rows in, the displaced rows
+//            out), U12 = L11^{-1} A12 (8 lanes, one column each), A22 -= L21 U12 on the FP64 tensor path
+//            (mma.sync.m8n8k4.f64 = DMMA; a complex 8x8x4 product is 4 real DMMAs), loads of a chunk of row tiles
+//            issued before its DMMAs.
+// Each warp runs its own task loop with no lock-step barriers: first the critical chain (bring its next panel up to
+// date and factor it as soon as the panels it needs are published), then the oldest ready backlog update, else it
+// polls the publish counter.  This is a lookahead of arbitrary depth: a panel is factored as soon as its column is
+// current, and the rest of the trailing update fills the gaps.
+// L is never stored for later use: B rides along as columns R..R+2, so forward elimination happens in the updates
+// and only U remains for the back substitution, which runs on one warp with the solution in registers (lane = row).
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "podp_common.cuh"
+
+namespace podp {
+
+namespace ludyn {
+
+constexpr int NB = 8;
+
+template <int R, int W>
+struct Cfg {
+  static_assert(R % 8 == 0, "R must be a multiple of 8 (exact padding)");
+  static constexpr int NPAN = R / NB;           // panels
+  static constexpr int NCP = R + 8;             // columns incl. the RHS tile (R..R+2 used)
+  static constexpr int NTC = NCP / 8;           // tile-columns (= NPAN + 1)
+  static constexpr int LDA = NCP + 1;           // row stride (complex), odd
+  static constexpr int MS = (R + 31) / 32;      // panel row slots per lane
+  static constexpr int NOWN = (NTC + W - 1) / W;  // tile-columns per warp (upper bound)
+  static constexpr int A_ELEMS = R * LDA;
+  // A, 1/U_kk (R), orig (R), dst (R), {published panels, info, pad}, pivot-row scratch (9)
+  // ... + one mbarrier per panel (completes when the panel is published)
+  // (rounded to 16 B so that every group's base stays aligned)
+  static constexpr int G_BYTES = (A_ELEMS * 16 + R * 16 + 2 * R * 4 + 16 + 9 * 16 + NPAN * 8 + 15) / 16 * 16;
+  static constexpr int GROUPS_SMEM = (225 * 1024) / G_BYTES;
+  static constexpr int GROUPS_T = (16 / W) < 15 ? (16 / W) : 15;  // <= 16 warps, one named barrier per group
+  static constexpr int GROUPS = GROUPS_SMEM < GROUPS_T ? GROUPS_SMEM : GROUPS_T;
+  static constexpr int THREADS = GROUPS * W * 32;
+  static constexpr size_t BYTES = (size_t)GROUPS * G_BYTES;
+  static_assert(GROUPS >= 1, "matrix does not fit in shared memory");
+};
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long *m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *m) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(m))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long *m, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"((unsigned)__cvta_generic_to_shared(m)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+// select without letting the compiler turn a slot choice into a dynamically indexed (local-memory) array
+__device__ __forceinline__ double selp(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}" : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)p));
+  return r;
+}
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+#ifndef PODP_LU_TRACE
+#define PODP_LU_TRACE 0
+#endif
+
+}  // namespace ludyn
+
+// dev instrumentation (build with -DPODP_LU_TRACE=1, run with PODP_LU_TRACE=1): per-task clock64 records of block 0,
+// group 0, frequencies 1 and 2 -- trace[(it-1)*2048 + w*256 + 3k + {0,1,2}] = {kind<<16 | b<<8 | tile, start, end}
+#define LD_TR_BEGIN() const long long tr_t0_ = PODP_LU_TRACE ? clock64() : 0
+#define LD_TR_END(kind, b, tc)                                                                                   \
+  do {                                                                                                           \
+    if constexpr (PODP_LU_TRACE)                                                                                 \
+      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && (it_ == 1 || it_ == 2) && ntr_ < 80) {       \
+        long long *tp = a.trace + (it_ - 1) * 2048 + w * 256 + 3 * ntr_++;                                      \
+        tp[0] = ((kind) << 16) | ((b) << 8) | (tc);                                                              \
+        tp[1] = tr_t0_;                                                                                          \
+        tp[2] = clock64();                                                                                       \
+      }                                                                                                          \
+  } while (0)
+
+
+namespace ludyn {
+
+// F: factor the panel at rows/cols kb.. (8 columns, rows kb..R-1) in registers; MS = row slots per lane needed for
+// the R - kb panel rows.  Rows never move: each lane tracks the current position of its rows (LAPACK interchange
+// semantics); the pivot search key carries the row's slot id (lowest id on ties); the pivot row is broadcast through
+// an 8-entry shared scratch row.  Returns the first zero-pivot info (0 if none).
+template <int R, int LDA, int MS>
+__device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOrig, int *sDst, double2 *sRow, int kb,
+                                            int lane, long long *ftr = nullptr) {
+#define FTR(k) \
+  if (PODP_LU_TRACE && ftr && lane == 0) ftr[k] = clock64()
+  FTR(0);
+  constexpr int NB = 8;
+  const unsigned FULL = 0xffffffffu;
+  double2 pn[MS][NB];
+  int pos[MS];
+#pragma unroll
+  for (int m = 0; m < MS; ++m) {
+    const int i = kb + lane + 32 * m;
+    pos[m] = i < R ? i : (1 << 20);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) pn[m][c] = (i < R) ? A[i * LDA + kb + c] : make_double2(0.0, 0.0);
+  }
+  int info = 0;
+  FTR(1);
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int kr = kb + j;
+    unsigned key = 0u;
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - (32 * m + lane));
+      if (pos[m] >= kr && pos[m] < R && kk > key) key = kk;
+    }
+    const unsigned best = __reduce_max_sync(FULL, key);
+    FTR(2 + 3 * j);
+    if ((best >> 7) == 0u) {  // exactly zero column (LAPACK getrf info = k+1); no interchange, no elimination
+      if (info == 0) info = kr + 1;
+      if (lane == 0) sRinv[kr] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const int id = 127 - (int)(best & 127u);
+    const int src = id & 31, ms = id >> 5;  // warp-uniform: lane and slot holding the pivot row
+    int p = 0;
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      if (m == ms && lane == src) {
+#pragma unroll
+        for (int c = j; c < NB; ++c) sRow[c] = pn[m][c];
+        sRow[NB] = make_double2(__hiloint2double(0, pos[m]), 0.0);
+      }
+    }
+    __syncwarp();
+    const double2 pv = sRow[j];
+    double2 u[NB];
+#pragma unroll
+    for (int c = j + 1; c < NB; ++c) u[c] = sRow[c];
+    p = __double2loint(sRow[NB].x);  // current position of the pivot row
+#pragma unroll
+    for (int m = 0; m < MS; ++m) pos[m] = (m == ms && lane == src) ? kr : (pos[m] == kr ? p : pos[m]);
+    FTR(3 + 3 * j);
+    const double2 rc = crecip_fast(pv);
+    if (lane == 0) sRinv[kr] = rc;
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const bool act = pos[m] > kr && pos[m] < R;
+      const double2 l = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
+      if (act) pn[m][j] = l;
+#pragma unroll
+      for (int c = j + 1; c < NB; ++c) pn[m][c] = cfms(l, u[c], pn[m][c]);
+    }
+    __syncwarp();  // scratch row reused by the next column
+    FTR(4 + 3 * j);
+  }
+  // write back (L21 multipliers, L11, U11) at the final positions and record the step's permutation
+#pragma unroll
+  for (int m = 0; m < MS; ++m) {
+    const int o = kb + lane + 32 * m;
+    if (pos[m] < R) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) A[pos[m] * LDA + kb + c] = pn[m][c];
+      if (pos[m] < kb + NB) sOrig[pos[m]] = o;
+      if (o < kb + NB) sDst[o] = pos[m];
+    }
+  }
+  __syncwarp();
+  FTR(26);
+  // L11^{-1} (unit lower) replaces L11 in its slots, so every U(b, .) forms U12 = L11^{-1} (P A12) on DMMA:
+  // lane c < 8 solves L11 y = e_c by forward substitution (zeros above c keep the code uniform)
+  if (lane < NB) {
+    const int c = lane;
+    double2 x[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) x[j] = make_double2(j == c ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int j = 1; j < NB; ++j) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int tt = 0; tt < j; ++tt) acc = cfma(A[(kb + j) * LDA + kb + tt], x[tt], acc);
+      if (j > c) x[j] = make_double2(-acc.x, -acc.y);
+    }
+#pragma unroll
+    for (int j = 1; j < NB; ++j)
+      if (j > c) A[(kb + j) * LDA + kb + c] = x[j];
+  }
+  FTR(27);
+#undef FTR
+  return info;
+}
+
+// U: apply the panel at kb to the tile-column at col0 (NRT = row tiles below the panel, compile-time).
+template <int R, int LDA, int NRT>
+__device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, const int *sDst, int kb, int col0,
+                                                int lane) {
+  constexpr int NB = 8;
+  // (1) permutation in one pass and U12 = L11^{-1} (P A12) on DMMA: the B-fragments of P A12 are read straight
+  //     from the pivot rows' pre-step locations; lanes (row j = lane / 4, two columns) move the displaced rows out.
+  {
+    const int arow = lane >> 2, acol = lane & 3;
+    const int bk = lane & 3, bcol = lane >> 2;
+    const int crow = lane >> 2, ccol = 2 * (lane & 3);
+    const double2 x0 = A[sOrig[kb + bk] * LDA + col0 + bcol], x1 = A[sOrig[kb + 4 + bk] * LDA + col0 + bcol];
+    const int dst = sDst[kb + crow];
+    const double2 o0 = A[(kb + crow) * LDA + col0 + ccol], o1 = A[(kb + crow) * LDA + col0 + ccol + 1];
+    const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
+    const double2 v0 = arow > acol ? A[(kb + arow) * LDA + kb + acol] : (arow == acol ? one : zero);
+    const double2 v1 = arow > acol + 4 ? A[(kb + arow) * LDA + kb + acol + 4] : (arow == acol + 4 ? one : zero);
+    __syncwarp();
+    if (dst >= kb + NB) {
+      A[dst * LDA + col0 + ccol] = o0;
+      A[dst * LDA + col0 + ccol + 1] = o1;
+    }
+    double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+    dmma(er0, er1, v0.x, x0.x);
+    dmma(ei0, ei1, v0.x, x0.y);
+    dmma(er0, er1, -v0.y, x0.y);
+    dmma(ei0, ei1, v0.y, x0.x);
+    dmma(er0, er1, v1.x, x1.x);
+    dmma(ei0, ei1, v1.x, x1.y);
+    dmma(er0, er1, -v1.y, x1.y);
+    dmma(ei0, ei1, v1.y, x1.x);
+    A[(kb + crow) * LDA + col0 + ccol] = make_double2(er0, ei0);
+    A[(kb + crow) * LDA + col0 + ccol + 1] = make_double2(er1, ei1);
+  }
+  __syncwarp();
+  if constexpr (NRT > 0) {
+    // (2) A22[:, tile] -= L21 U12[:, tile]: all fragment loads of a chunk of row tiles before its DMMAs
+    constexpr int CH = NRT < 5 ? NRT : 5;
+    const int arow = lane >> 2, acol = lane & 3;
+    const int bk = lane & 3, bcol = lane >> 2;
+    const int crow = lane >> 2, ccol = 2 * (lane & 3);
+    const double2 b0 = A[(kb + bk) * LDA + col0 + bcol], b1 = A[(kb + 4 + bk) * LDA + col0 + bcol];
+#pragma unroll
+    for (int t0 = 0; t0 < NRT; t0 += CH) {
+      double2 a0[CH], a1[CH], c0[CH], c1[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        if (t0 + q < NRT) {
+          const int tr = kb + NB + 8 * (t0 + q);
+          a0[q] = A[(tr + arow) * LDA + kb + acol];
+          a1[q] = A[(tr + arow) * LDA + kb + 4 + acol];
+          c0[q] = A[(tr + crow) * LDA + col0 + ccol];
+          c1[q] = A[(tr + crow) * LDA + col0 + ccol + 1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        if (t0 + q < NRT) {
+          double cr0 = c0[q].x, cr1 = c1[q].x, ci0 = c0[q].y, ci1 = c1[q].y;
+          // C -= A B (complex): C_re += (-A_re) B_re + A_im B_im ; C_im += (-A_re) B_im + (-A_im) B_re
+          dmma(cr0, cr1, -a0[q].x, b0.x);
+          dmma(ci0, ci1, -a0[q].x, b0.y);
+          dmma(cr0, cr1, a0[q].y, b0.y);
+          dmma(ci0, ci1, -a0[q].y, b0.x);
+          dmma(cr0, cr1, -a1[q].x, b1.x);
+          dmma(ci0, ci1, -a1[q].x, b1.y);
+          dmma(cr0, cr1, a1[q].y, b1.y);
+          dmma(ci0, ci1, -a1[q].y, b1.x);
+          c0[q] = make_double2(cr0, ci0);
+          c1[q] = make_double2(cr1, ci1);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        if (t0 + q < NRT) {
+          const int tr = kb + NB + 8 * (t0 + q);
+          A[(tr + crow) * LDA + col0 + ccol] = c0[q];
+          A[(tr + crow) * LDA + col0 + ccol + 1] = c1[q];
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int R, int LDA, int N = R / 8 - 1>
+__device__ __forceinline__ void update_dispatch(double2 *A, const int *sOrig, const int *sDst, int b, int col0,
+                                                int lane) {
+  // NRT = R/8 - 1 - b: one instantiation per panel index keeps every loop bound and offset compile-time
+  if (R / 8 - 1 - b == N) {
+    update_tile_col<R, LDA, N>(A, sOrig, sDst, b * 8, col0, lane);
+  } else if constexpr (N > 0) {
+    update_dispatch<R, LDA, N - 1>(A, sOrig, sDst, b, col0, lane);
+  }
+}
+
+}  // namespace ludyn
+
+template <int R, int W>
+__global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(EvalArgs a) {
+  using C = ludyn::Cfg<R, W>;
+  constexpr int NTC = C::NTC, LDA = C::LDA, MS = C::MS, NB = ludyn::NB, NT = W * 32, NPAN = C::NPAN;
+  constexpr int NOWN = C::NOWN;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = wid / W, w = wid % W;
+  unsigned char *gbase = smem_raw + (size_t)grp * C::G_BYTES;
+  double2 *A = reinterpret_cast<double2 *>(gbase);
+  double2 *sRinv = A + C::A_ELEMS;
+  int *sOrig = reinterpret_cast<int *>(sRinv + R);  // sOrig[q]: pre-step position of the row now at q (q in panel)
+  int *sDst = sOrig + R;                             // sDst[o]: final position of the row that was at o (o in panel)
+  int *sPub = sDst + R;                              // [0] panels published, [1] info
+  double2 *sRow = reinterpret_cast<double2 *>(sPub + 4);  // pivot-row scratch (8 values + position)
+  unsigned long long *sBar = reinterpret_cast<unsigned long long *>(sRow + 9);  // [NPAN] publish mbarriers
+  if (w == 0 && lane == 0)
+    for (int k = 0; k < NPAN; ++k) ludyn::mbar_init(sBar + k, 1);
+  __syncthreads();
+  unsigned lu_par = 0;  // phase parity of the publish mbarriers (flips once per factorised frequency)
+  const int bar_id = 1 + grp;
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+  const int ngroups_total = gridDim.x * C::GROUPS;
+  int it_ = -1, ntr_ = 0;
+  (void)ntr_;
+
+  for (int64_t t = (int64_t)blockIdx.x * C::GROUPS + grp; t < total; t += ngroups_total) {
+    const int obj = (int)(t / a.F);
+    const int64_t f = t - (int64_t)obj * a.F;
+    const double *op = a.ops + (size_t)obj * a.L.stride;
+    const double om = a.omega[f];
+    const double s = om * op[a.L.scal + SC_NU];
+    ++it_;
+    ntr_ = 0;
+    LD_TR_BEGIN();
+    // ---- a2: assemble [A | B | 0] (all W warps).  K is copied into A by cp.async (16 B per element, all copies in
+    //      flight at once, no registers); M is streamed through registers in two batches meanwhile; each thread
+    //      then adds i s M to the K entries it copied itself (cp.async.wait_all orders its own copies). ------------
+    {
+      const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
+      const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
+      constexpr int PER = (R * R + NT - 1) / NT;
+      constexpr int HALF = (PER + 1) / 2;
+      const int gl = w * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int e = q * NT + gl;
+        if (e < R * R) {
+          const int i = e / R, j = e - i * R;
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(A + i * LDA + j);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gK + e) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
+      const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
+#pragma unroll
+      for (int q = 0; q < (8 * R + NT - 1) / NT; ++q) {
+        const int e = q * NT + gl;
+        if (e >= 8 * R) break;
+        const int i = e >> 3, c = e & 7;
+        double2 v = make_double2(0.0, 0.0);
+        if (c < 3) {
+          const double2 x0 = __ldg(gb0 + c * R + i), x1 = __ldg(gb1 + c * R + i);
+          v = make_double2(fma(om, x1.x, x0.x), fma(om, x1.y, x0.y));
+        }
+        A[i * LDA + R + c] = v;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 mm[HALF];
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+          const int e = (h * HALF + q) * NT + gl;
+          if (h * HALF + q < PER && e < R * R) mm[q] = __ldg(gM + e);
+        }
+        if (h == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < HALF; ++q) {
+          const int e = (h * HALF + q) * NT + gl;
+          if (h * HALF + q < PER && e < R * R) {
+            const int i = e / R, j = e - i * R;
+            const double2 kk = A[i * LDA + j];
+            A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk.x), fma(s, mm[q].x, kk.y));
+          }
+        }
+      }
+      if (w == 0 && lane == 0) {
+        sPub[0] = 0;
+        sPub[1] = isfinite(om) ? 0 : -1;
+      }
+    }
+    if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
+    LD_TR_END(0, 0, 0);
+    // ---- a3: dynamically scheduled blocked LU ------------------------------------------------------------------------
+    const bool lu_run = sPub[1] == 0;
+    if (lu_run) {
+      int done[NOWN];  // updates applied to each owned tile-column (tile w + q W)
+#pragma unroll
+      for (int q = 0; q < NOWN; ++q) done[q] = 0;
+      int nf = w;       // next panel this warp factors (tile index; >= NPAN: none left)
+      int pub = 0;      // panels known to be published
+      unsigned spins = 0;
+      for (;;) {
+        // pick the next task: (1) the critical chain -- bring the next own panel up to date and factor it;
+        // (2) else the owned tile-column with the fewest applied panels among the ready ones; (3) else poll.
+        int ub = -1, uq = -1;  // update task U(ub, tile w + uq W)
+        if (nf < NPAN) {
+          int dn = 0, qn = 0;
+#pragma unroll
+          for (int q = 0; q < NOWN; ++q)
+            if (w + q * W == nf) {
+              dn = done[q];
+              qn = q;
+            }
+          if (dn == nf) {
+            LD_TR_BEGIN();
+            long long *ftr = (PODP_LU_TRACE && a.trace && blockIdx.x == 0 && grp == 0 && (it_ == 1 || it_ == 2))
+                                 ? a.trace + 4096 + (it_ - 1) * 1024 + nf * 32
+                                 : nullptr;
+            const int inf = (R - nf * NB > 32)
+                                ? ludyn::factor_panel<R, LDA, MS>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane, ftr)
+                                : ludyn::factor_panel<R, LDA, 1>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane, ftr);
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) {
+              if (inf != 0 && sPub[1] == 0) sPub[1] = inf;
+              ludyn::st_release(sPub, nf + 1);
+              ludyn::mbar_arrive(sBar + nf);
+            }
+            LD_TR_END(1, nf, nf);
+            if (nf + 1 > pub) pub = nf + 1;
+            nf += W;
+            continue;
+          }
+          if (dn >= pub) pub = ludyn::ld_acquire(sPub);
+          if (dn < pub) {
+            ub = dn;
+            uq = qn;
+          }
+        }
+        if (uq < 0) {
+          int best_d = 1 << 20;
+          bool all = nf >= NPAN;
+#pragma unroll
+          for (int q = 0; q < NOWN; ++q) {
+            const int tc = w + q * W;
+            if (tc < NTC) {
+              const int lim = tc < NPAN ? tc : NPAN;
+              if (done[q] < lim) {
+                all = false;
+                if (!(nf < NPAN && tc == nf) && done[q] < pub && done[q] < best_d) {
+                  best_d = done[q];
+                  uq = q;
+                }
+              }
+            }
+          }
+          if (all) break;
+          if (uq < 0) {
+            // nothing ready: block (hardware-suspended try_wait) until the next panel is published
+            while (!ludyn::mbar_try_wait(sBar + pub, lu_par))
+              if (++spins > (1 << 24)) __trap();  // scheduling invariant broken: fail loudly instead of hanging
+            pub = ludyn::ld_acquire(sPub);
+            continue;
+          }
+          ub = best_d;
+        }
+        {
+          LD_TR_BEGIN();
+          ludyn::update_dispatch<R, LDA>(A, sOrig, sDst, ub, (w + uq * W) * 8, lane);
+          LD_TR_END(2, ub, w + uq * W);
+        }
+#pragma unroll
+        for (int q = 0; q < NOWN; ++q)
+          if (q == uq) done[q] += 1;
+      }
+    }
+    {
+      LD_TR_BEGIN();
+      if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
+      LD_TR_END(3, 0, 0);
+    }
+    if (lu_run) lu_par ^= 1u;
+    const int info = sPub[1];
+    const long long tr_bs_ = PODP_LU_TRACE ? clock64() : 0;
+    // ---- back substitution U x = y, blocked and left-looking on the FP64 tensor path.
+    //      (i) all W warps invert the NPAN diagonal 8x8 blocks of U (one lane per block column; the strictly upper
+    //      part of each inverse is stored transposed in the dead L11 slots, its diagonal is 1/U_kk);
+    //      (ii) warp 0, for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), then
+    //      x_b = Dinv_b y_b (DMMA).  The right-hand-side tile (8 columns, 3 used) is the DMMA n dimension.
+    double2 *Pw = a.Pws + (size_t)t * 3 * R;
+    if (info == 0) {
+      for (int task = w * 32 + lane; task < NPAN * 8; task += NT) {
+        const int kb = (task >> 3) * 8, c = task & 7;
+        double2 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+          if (j == c) x[j] = sRinv[kb + j];
+          if (j < c) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int tt = j + 1; tt < 8; ++tt)
+              if (tt <= c) acc = cfma(A[(kb + j) * LDA + kb + tt], x[tt], acc);
+            x[j] = cmul(make_double2(-acc.x, -acc.y), sRinv[kb + j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < c) A[(kb + c) * LDA + kb + j] = x[j];  // Dinv[j][c] stored at (c, j)
+      }
+      if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
+    }
+    if (w == 0) {
+      if (info == 0) {
+        const int arow = lane >> 2, acol = lane & 3;
+        const int bk = lane & 3, bcol = lane >> 2;
+        const int crow = lane >> 2, ccol = 2 * (lane & 3);
+        for (int b = NPAN - 1; b >= 0; --b) {
+          const int kb = b * 8;
+          double2 y0 = A[(kb + crow) * LDA + R + ccol], y1 = A[(kb + crow) * LDA + R + ccol + 1];
+          double cr0 = y0.x, cr1 = y1.x, ci0 = y0.y, ci1 = y1.y;
+          double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
+          for (int bb = b + 1; bb < NPAN; ++bb) {
+            const int kc = bb * 8;
+            const double2 a0 = A[(kb + arow) * LDA + kc + acol], a1 = A[(kb + arow) * LDA + kc + 4 + acol];
+            const double2 x0 = A[(kc + bk) * LDA + R + bcol], x1 = A[(kc + 4 + bk) * LDA + R + bcol];
+            if ((bb - b) & 1) {
+              ludyn::dmma(cr0, cr1, -a0.x, x0.x);
+              ludyn::dmma(ci0, ci1, -a0.x, x0.y);
+              ludyn::dmma(cr0, cr1, a0.y, x0.y);
+              ludyn::dmma(ci0, ci1, -a0.y, x0.x);
+              ludyn::dmma(cr0, cr1, -a1.x, x1.x);
+              ludyn::dmma(ci0, ci1, -a1.x, x1.y);
+              ludyn::dmma(cr0, cr1, a1.y, x1.y);
+              ludyn::dmma(ci0, ci1, -a1.y, x1.x);
+            } else {
+              ludyn::dmma(dr0, dr1, -a0.x, x0.x);
+              ludyn::dmma(di0, di1, -a0.x, x0.y);
+              ludyn::dmma(dr0, dr1, a0.y, x0.y);
+              ludyn::dmma(di0, di1, -a0.y, x0.x);
+              ludyn::dmma(dr0, dr1, -a1.x, x1.x);
+              ludyn::dmma(di0, di1, -a1.x, x1.y);
+              ludyn::dmma(dr0, dr1, a1.y, x1.y);
+              ludyn::dmma(di0, di1, -a1.y, x1.x);
+            }
+          }
+          __syncwarp();
+          A[(kb + crow) * LDA + R + ccol] = make_double2(cr0 + dr0, ci0 + di0);
+          A[(kb + crow) * LDA + R + ccol + 1] = make_double2(cr1 + dr1, ci1 + di1);
+          __syncwarp();
+          // x_b = Dinv_b y_b: A-fragment of the upper-triangular inverse from its transposed storage
+          double2 v0, v1;
+          {
+            const int m = arow, k0 = acol, k1 = acol + 4;
+            v0 = m < k0 ? A[(kb + k0) * LDA + kb + m] : (m == k0 ? sRinv[kb + m] : make_double2(0.0, 0.0));
+            v1 = m < k1 ? A[(kb + k1) * LDA + kb + m] : (m == k1 ? sRinv[kb + m] : make_double2(0.0, 0.0));
+          }
+          const double2 x0 = A[(kb + bk) * LDA + R + bcol], x1 = A[(kb + 4 + bk) * LDA + R + bcol];
+          double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+          ludyn::dmma(er0, er1, v0.x, x0.x);
+          ludyn::dmma(ei0, ei1, v0.x, x0.y);
+          ludyn::dmma(er0, er1, -v0.y, x0.y);
+          ludyn::dmma(ei0, ei1, v0.y, x0.x);
+          ludyn::dmma(er0, er1, v1.x, x1.x);
+          ludyn::dmma(ei0, ei1, v1.x, x1.y);
+          ludyn::dmma(er0, er1, -v1.y, x1.y);
+          ludyn::dmma(ei0, ei1, v1.y, x1.x);
+          __syncwarp();
+          A[(kb + crow) * LDA + R + ccol] = make_double2(er0, ei0);
+          A[(kb + crow) * LDA + R + ccol + 1] = make_double2(er1, ei1);
+          __syncwarp();
+        }
+        for (int e = lane; e < 3 * R; e += 32) {
+          const int c = e / R, i = e - c * R;
+          const double2 v = A[i * LDA + R + c];
+          Pw[e] = v;
+          if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = v;
+        }
+      } else {
+        for (int e = lane; e < 3 * R; e += 32) Pw[e] = make_double2(nanv, nanv);
+        if (a.P_out)
+          for (int e = lane; e < 3 * a.r; e += 32)
+            reinterpret_cast<double2 *>(a.P_out)[(size_t)t * 3 * a.r + e] = make_double2(nanv, nanv);
+      }
+      if (a.info && lane == 0) a.info[t] = info;
+      {
+        const long long tr_t0_ = tr_bs_;
+        LD_TR_END(4, 0, 0);
+      }
+    }
+    if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
+  }
+}
+
+template <int R, int W>
+static cudaError_t launch_lu_dyn_t(const EvalArgs &a, cudaStream_t s) {
+  using C = ludyn::Cfg<R, W>;
+  auto kern = lu_dyn_kernel<R, W>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  int64_t blocks = (total + C::GROUPS - 1) / C::GROUPS;
+  if (blocks > sms) blocks = sms;
+  kern<<<(unsigned)blocks, C::THREADS, C::BYTES, s>>>(a);
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess && getenv("PODP_LU_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "lu_dyn<%d,%d>: threads %d bytes %zu regs %d maxThreads %d local %zu\n", R, W, C::THREADS,
+            C::BYTES, fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes);
+  }
+  return le;
+}
+
+cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
+  if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
+  const char *v = getenv("PODP_LU_W");
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48 and 72, four
+  // at R = 56, 64 and 80..96
+  const int R = a.L.R;
+  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 72) ? 2 : 4));
+  switch (R) {
+#define PODP_CASE(RR)                                     \
+  case RR:                                                \
+    if (wv == 1) return launch_lu_dyn_t<RR, 1>(a, s);     \
+    if (wv == 2) return launch_lu_dyn_t<RR, 2>(a, s);     \
+    return launch_lu_dyn_t<RR, 4>(a, s);
+#ifdef PODP_DEV_R  // dev builds: a single instantiation
+    case PODP_DEV_R: return launch_lu_dyn_t<PODP_DEV_R, PODP_DEV_W>(a, s);
+#else
+    PODP_CASE(8)
+    PODP_CASE(16)
+    PODP_CASE(24)
+    PODP_CASE(32)
+    PODP_CASE(40)
+    PODP_CASE(48)
+    PODP_CASE(56)
+    PODP_CASE(64)
+    PODP_CASE(72)
+    PODP_CASE(80)
+    PODP_CASE(88)
+    PODP_CASE(96)
+#endif
+#undef PODP_CASE
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace podp

@@ -485,6 +485,7 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   if (getenv("PODP_LU_TRACE")) {
     if (!trace_buf) cudaMallocManaged(&trace_buf, 8 * 1024 * sizeof(long long));
     cudaMemset(trace_buf, 0, 8 * 1024 * sizeof(long long));
+    cudaDeviceSynchronize();
     a.trace = trace_buf;
   }
   const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
@@ -506,13 +507,17 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   }
   {
     ProfScope ps("solve", s);
-    const char *lv = getenv("PODP_LU_IMPL");  // dev switch: "reg" = register-resident kernel, default blocked
+    // default LU kernel per padded R, measured on B200 (tools/lu_ab.py): the lock-step blocked kernel at R = 8, 16, 48
+    // and 64, the dynamically scheduled one elsewhere; dev switch PODP_LU_IMPL = b | d | r forces one
+    const char *lv = getenv("PODP_LU_IMPL");
+    const int R = c->L.R;
+    const bool use_blk = lv ? lv[0] == 'b' : (R == 8 || R == 16 || R == 48 || R == 64);
     if ((flags & PODP_FLAG_PENCIL) && pencil_y) e = podp::launch_pencil_y(a, s);
     else if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
     else if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
     else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
-    else if (lv && lv[0] == 'p') e = podp::launch_lu_pw(a, s);
-    else e = podp::launch_lu_blk(a, s);
+    else if (use_blk) e = podp::launch_lu_blk(a, s);
+    else e = podp::launch_lu_dyn(a, s);
     if (e == cudaSuccess) {
       ++nl;
     } else if (e == cudaErrorNotSupported) {
@@ -540,7 +545,35 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   }
   cudaFreeAsync(a.Pws, s);
   g_last_launches = nl;
-  if (a.trace) {  // dev instrumentation dump (build with PODP_NVCC_EXTRA=-DPODP_LU_TRACE=1)
+  if (a.trace && getenv("PODP_LU_IMPL") && getenv("PODP_LU_IMPL")[0] == 'd') {  // lu_dyn task records (dev)
+    cudaDeviceSynchronize();
+    const char *kinds[] = {"assemble", "F", "U", "bar", "backsub"};
+    for (int it = 0; it < 2; ++it) {
+      long long t0 = 0;
+      for (int w = 0; w < 8; ++w) {
+        const long long *tr = trace_buf + it * 2048 + w * 256;
+        if (tr[1] && (!t0 || tr[1] < t0)) t0 = tr[1];
+      }
+      for (int w = 0; w < 8; ++w) {
+        const long long *tr = trace_buf + it * 2048 + w * 256;
+        if (!tr[1]) continue;
+        fprintf(stderr, "omega %d warp %d:", it + 1, w);
+        for (int k = 0; k < 80 && tr[3 * k + 1]; ++k) {
+          const long long c = tr[3 * k];
+          fprintf(stderr, " %s(%lld,%lld)[%lld-%lld]", kinds[(c >> 16) & 7], (c >> 8) & 255, c & 255, tr[3 * k + 1] - t0, tr[3 * k + 2] - t0);
+        }
+        fprintf(stderr, "\n");
+      }
+      for (int k = 0; k < 16; ++k) {  // F internals: load | per column: redux, bcast, end | write-back | L11inv
+        const long long *ft = trace_buf + 4096 + it * 1024 + k * 32;
+        if (!ft[0]) continue;
+        fprintf(stderr, "  F%d: load %lld |", k, ft[1] - ft[0]);
+        for (int j = 0; j < 8; ++j)
+          fprintf(stderr, " c%d %lld/%lld/%lld", j, ft[2 + 3 * j] - ft[0], ft[3 + 3 * j] - ft[0], ft[4 + 3 * j] - ft[0]);
+        fprintf(stderr, " | wb %lld | inv %lld\n", ft[26] - ft[0], ft[27] - ft[0]);
+      }
+    }
+  } else if (a.trace) {  // dev instrumentation dump (build with PODP_NVCC_EXTRA=-DPODP_LU_TRACE=1)
     cudaDeviceSynchronize();
     for (int q = 1; q < 3; ++q) {
       const long long *tr = trace_buf + q * 1024;

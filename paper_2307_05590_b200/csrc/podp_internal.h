@@ -50,7 +50,7 @@ struct EvalArgs {
 cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag = false);  // NotSupported if no instantiation
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
-cudaError_t launch_lu_pw(const EvalArgs &a, cudaStream_t s);     // cudaErrorNotSupported if no instantiation
+cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
 cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
 cudaError_t launch_pencil_y(const EvalArgs &a, cudaStream_t s);  // N3: y = (I + i s Lambda)^{-1}(c0 + omega c1) only
 cudaError_t launch_invariants(const double *T1, const double *I, int64_t n, double *eigR, double *eigI, cudaStream_t s);

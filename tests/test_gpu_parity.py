@@ -159,6 +159,25 @@ def test_edge_cases_fast_path(torch_cuda, r):
     assert list(res["info"][0]) == [6, 6]
 
 
+@pytest.mark.parametrize("impl", ["b", "d"])
+@pytest.mark.parametrize("r", [8, 24, 40, 48, 72, 96])
+def test_both_lu_kernels_parity_and_singular(torch_cuda, monkeypatch, impl, r):
+    """Both LU kernels (lock-step blocked 'b', dynamically scheduled 'd'; the default picks one per padded R) stay
+    parity-green on every size class, including a zero pivot at a later panel (LAPACK info = k+1)."""
+    monkeypatch.setenv("PODP_LU_IMPL", impl)
+    ops = g.make_operators(r, seed=r + 1)
+    omega = np.r_[g.omega_grid(61), [np.inf]]
+    res = run_gpu(torch_cuda, ops, omega)
+    assert (res["info"][0][:61] == 0).all() and res["info"][0][61] == -1
+    check_parity(ops, omega, res, sample=range(61))
+    d = np.arange(1.0, r + 1)
+    k0 = min(r - 1, 13)
+    d[k0] = 0.0
+    z = g.Operators(**{**ops.__dict__, "K": np.diag(d).astype(complex), "M": np.zeros((r, r), complex)})
+    res = run_gpu(torch_cuda, z, np.array([1.0, 2.0]))
+    assert list(res["info"][0]) == [k0 + 1, k0 + 1] and np.isnan(res["T1"]).all()
+
+
 def test_invariants_scaling_bitwise(torch_cuda):
     """Remark 6.2, pin C8 on the GPU path: power-of-two scaling is exact -> bitwise."""
     o = g.make_operators(24)
