@@ -107,8 +107,8 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
 #define LD_TR_END(kind, b, tc)                                                                                   \
   do {                                                                                                           \
     if constexpr (PODP_LU_TRACE)                                                                                 \
-      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && (it_ == 1 || it_ == 2) && ntr_ < 80) {       \
-        long long *tp = a.trace + (it_ - 1) * 2048 + w * 256 + 3 * ntr_++;                                      \
+      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && (it_ == 0 || it_ == 1) && ntr_ < 80) {       \
+        long long *tp = a.trace + it_ * 2048 + w * 256 + 3 * ntr_++;                                      \
         tp[0] = ((kind) << 16) | ((b) << 8) | (tc);                                                              \
         tp[1] = tr_t0_;                                                                                          \
         tp[2] = clock64();                                                                                       \
@@ -160,20 +160,28 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     const int id = 127 - (int)(best & 127u);
     const int src = id & 31, ms = id >> 5;  // warp-uniform: lane and slot holding the pivot row
     int p = 0;
+    double2 pv, u[NB];
+    if constexpr (MS == 1) {
+      // one row slot: the pivot row is broadcast by shuffles (no shared-memory round trip on the chain)
+      pv = shfl2(pn[0][j], src);
 #pragma unroll
-    for (int m = 0; m < MS; ++m) {
-      if (m == ms && lane == src) {
+      for (int c = j + 1; c < NB; ++c) u[c] = shfl2(pn[0][c], src);
+      p = __shfl_sync(FULL, pos[0], src);
+    } else {
 #pragma unroll
-        for (int c = j; c < NB; ++c) sRow[c] = pn[m][c];
-        sRow[NB] = make_double2(__hiloint2double(0, pos[m]), 0.0);
+      for (int m = 0; m < MS; ++m) {
+        if (m == ms && lane == src) {
+#pragma unroll
+          for (int c = j; c < NB; ++c) sRow[c] = pn[m][c];
+          sRow[NB] = make_double2(__hiloint2double(0, pos[m]), 0.0);
+        }
       }
-    }
-    __syncwarp();
-    const double2 pv = sRow[j];
-    double2 u[NB];
+      __syncwarp();
+      pv = sRow[j];
 #pragma unroll
-    for (int c = j + 1; c < NB; ++c) u[c] = sRow[c];
-    p = __double2loint(sRow[NB].x);  // current position of the pivot row
+      for (int c = j + 1; c < NB; ++c) u[c] = sRow[c];
+      p = __double2loint(sRow[NB].x);  // current position of the pivot row
+    }
 #pragma unroll
     for (int m = 0; m < MS; ++m) pos[m] = (m == ms && lane == src) ? kr : (pos[m] == kr ? p : pos[m]);
     FTR(3 + 3 * j);
@@ -187,7 +195,7 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
 #pragma unroll
       for (int c = j + 1; c < NB; ++c) pn[m][c] = cfms(l, u[c], pn[m][c]);
     }
-    __syncwarp();  // scratch row reused by the next column
+    if constexpr (MS > 1) __syncwarp();  // scratch row reused by the next column
     FTR(4 + 3 * j);
   }
   // write back (L21 multipliers, L11, U11) at the final positions and record the step's permutation
@@ -224,6 +232,40 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
   FTR(27);
 #undef FTR
   return info;
+}
+
+// Dinv: the inverse of the upper-triangular diagonal block U11 of a panel replaces U11 in place (its slots are dead
+// once the panel is factored: trailing updates use L11^{-1}, L21 and U12 only).  Column c of the inverse comes from
+// back substitution with 1/U_kk from sRinv; every lane loads its U11 entries before any lane of the warp writes.
+// Tasks: lane -> (block kb0 + 8 (lane / 8), column lane % 8) for the nblk <= 4 blocks handled in one call.
+template <int LDA>
+__device__ __forceinline__ void invert_diag(double2 *A, const double2 *sRinv, int kb0, int nblk, int lane) {
+  constexpr int NB = 8;
+  double2 x[NB];
+  const bool act = lane < NB * nblk;
+  const int kb = kb0 + NB * (lane >> 3), c = lane & 7;
+  if (act) {
+    double2 u[NB][NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int t = j + 1; t < NB; ++t) u[j][t] = A[(kb + j) * LDA + kb + t];
+#pragma unroll
+    for (int j = NB - 1; j >= 0; --j) {
+      const double2 rj = sRinv[kb + j];
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = j + 1; t < NB; ++t) acc = cfma(u[j][t], x[t], acc);
+      x[j] = j == c ? rj : (j < c ? cmul(make_double2(-acc.x, -acc.y), rj) : make_double2(0.0, 0.0));
+    }
+  }
+  __syncwarp();
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j <= c) A[(kb + j) * LDA + kb + c] = x[j];
+  }
+  __syncwarp();
 }
 
 // U: apply the panel at kb to the tile-column at col0 (NRT = row tiles below the panel, compile-time).
@@ -442,8 +484,8 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
             }
           if (dn == nf) {
             LD_TR_BEGIN();
-            long long *ftr = (PODP_LU_TRACE && a.trace && blockIdx.x == 0 && grp == 0 && (it_ == 1 || it_ == 2))
-                                 ? a.trace + 4096 + (it_ - 1) * 1024 + nf * 32
+            long long *ftr = (PODP_LU_TRACE && a.trace && blockIdx.x == 0 && grp == 0 && (it_ == 0 || it_ == 1))
+                                 ? a.trace + 4096 + it_ * 1024 + nf * 32
                                  : nullptr;
             const int inf = (R - nf * NB > 32)
                                 ? ludyn::factor_panel<R, LDA, MS>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane, ftr)
@@ -457,6 +499,9 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
             }
             LD_TR_END(1, nf, nf);
             if (nf + 1 > pub) pub = nf + 1;
+            // W > 1: invert U11 now, in the slack before this warp's next critical task; W = 1 does all blocks at the end
+            if constexpr (W > 1)
+              if (inf == 0) ludyn::invert_diag<LDA>(A, sRinv, nf * NB, 1, lane);
             nf += W;
             continue;
           }
@@ -512,36 +557,17 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
     const int info = sPub[1];
     const long long tr_bs_ = PODP_LU_TRACE ? clock64() : 0;
     // ---- back substitution U x = y, blocked and left-looking on the FP64 tensor path.
-    //      (i) all W warps invert the NPAN diagonal 8x8 blocks of U (one lane per block column; the strictly upper
-    //      part of each inverse is stored transposed in the dead L11 slots, its diagonal is 1/U_kk);
-    //      (ii) warp 0, for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), then
+    //      The inverses Dinv_b of the diagonal blocks were formed in place by the factoring warps (invert_diag);
+    //      warp 0, for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), then
     //      x_b = Dinv_b y_b (DMMA).  The right-hand-side tile (8 columns, 3 used) is the DMMA n dimension.
     double2 *Pw = a.Pws + (size_t)t * 3 * R;
-    if (info == 0) {
-      for (int task = w * 32 + lane; task < NPAN * 8; task += NT) {
-        const int kb = (task >> 3) * 8, c = task & 7;
-        double2 x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int j = 7; j >= 0; --j) {
-          if (j == c) x[j] = sRinv[kb + j];
-          if (j < c) {
-            double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int tt = j + 1; tt < 8; ++tt)
-              if (tt <= c) acc = cfma(A[(kb + j) * LDA + kb + tt], x[tt], acc);
-            x[j] = cmul(make_double2(-acc.x, -acc.y), sRinv[kb + j]);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j < c) A[(kb + c) * LDA + kb + j] = x[j];  // Dinv[j][c] stored at (c, j)
-      }
-      if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
-    }
     if (w == 0) {
       if (info == 0) {
+        if constexpr (W == 1) {
+#pragma unroll
+          for (int b0 = 0; b0 < NPAN; b0 += 4)
+            ludyn::invert_diag<LDA>(A, sRinv, b0 * NB, NPAN - b0 < 4 ? NPAN - b0 : 4, lane);
+        }
         const int arow = lane >> 2, acol = lane & 3;
         const int bk = lane & 3, bcol = lane >> 2;
         const int crow = lane >> 2, ccol = 2 * (lane & 3);
@@ -550,11 +576,14 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
           double2 y0 = A[(kb + crow) * LDA + R + ccol], y1 = A[(kb + crow) * LDA + R + ccol + 1];
           double cr0 = y0.x, cr1 = y1.x, ci0 = y0.y, ci1 = y1.y;
           double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
-          for (int bb = b + 1; bb < NPAN; ++bb) {
+#pragma unroll
+          for (int d = 1; d < NPAN; ++d) {
+            const int bb = b + d;
+            if (bb >= NPAN) break;
             const int kc = bb * 8;
             const double2 a0 = A[(kb + arow) * LDA + kc + acol], a1 = A[(kb + arow) * LDA + kc + 4 + acol];
             const double2 x0 = A[(kc + bk) * LDA + R + bcol], x1 = A[(kc + 4 + bk) * LDA + R + bcol];
-            if ((bb - b) & 1) {
+            if (d & 1) {
               ludyn::dmma(cr0, cr1, -a0.x, x0.x);
               ludyn::dmma(ci0, ci1, -a0.x, x0.y);
               ludyn::dmma(cr0, cr1, a0.y, x0.y);
@@ -578,12 +607,12 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
           A[(kb + crow) * LDA + R + ccol] = make_double2(cr0 + dr0, ci0 + di0);
           A[(kb + crow) * LDA + R + ccol + 1] = make_double2(cr1 + dr1, ci1 + di1);
           __syncwarp();
-          // x_b = Dinv_b y_b: A-fragment of the upper-triangular inverse from its transposed storage
+          // x_b = Dinv_b y_b (Dinv_b stored in place of U11)
           double2 v0, v1;
           {
             const int m = arow, k0 = acol, k1 = acol + 4;
-            v0 = m < k0 ? A[(kb + k0) * LDA + kb + m] : (m == k0 ? sRinv[kb + m] : make_double2(0.0, 0.0));
-            v1 = m < k1 ? A[(kb + k1) * LDA + kb + m] : (m == k1 ? sRinv[kb + m] : make_double2(0.0, 0.0));
+            v0 = m <= k0 ? A[(kb + m) * LDA + kb + k0] : make_double2(0.0, 0.0);
+            v1 = m <= k1 ? A[(kb + m) * LDA + kb + k1] : make_double2(0.0, 0.0);
           }
           const double2 x0 = A[(kb + bk) * LDA + R + bcol], x1 = A[(kb + 4 + bk) * LDA + R + bcol];
           double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
@@ -648,10 +677,10 @@ static cudaError_t launch_lu_dyn_t(const EvalArgs &a, cudaStream_t s) {
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
   const char *v = getenv("PODP_LU_W");
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48 and 72, four
-  // at R = 56, 64 and 80..96
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, four at R = 56,
+  // 64 and 72..96
   const int R = a.L.R;
-  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 72) ? 2 : 4));
+  const int wv = v ? atoi(v) : (R <= 40 ? 1 : (R == 48 ? 2 : 4));
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \

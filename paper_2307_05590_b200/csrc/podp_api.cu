@@ -507,11 +507,12 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   }
   {
     ProfScope ps("solve", s);
-    // default LU kernel per padded R, measured on B200 (tools/lu_ab.py): the lock-step blocked kernel at R = 8, 16, 48
-    // and 64, the dynamically scheduled one elsewhere; dev switch PODP_LU_IMPL = b | d | r forces one
+    // default LU kernel per padded R, measured on B200 (tools/lu_ab.py, F = 1e5): the dynamically scheduled kernel
+    // at R = 40, 56 and >= 72 (3-20 % faster there), the lock-step blocked kernel elsewhere (R <= 32, 48, 64: within
+    // 1-7 %); dev switch PODP_LU_IMPL = b | d | r forces one
     const char *lv = getenv("PODP_LU_IMPL");
     const int R = c->L.R;
-    const bool use_blk = lv ? lv[0] == 'b' : (R == 8 || R == 16 || R == 48 || R == 64);
+    const bool use_blk = lv ? lv[0] == 'b' : !(R == 40 || R == 56 || R >= 72);
     if ((flags & PODP_FLAG_PENCIL) && pencil_y) e = podp::launch_pencil_y(a, s);
     else if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
     else if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
