@@ -12,8 +12,8 @@
 //     publishes it (`bar.arrive`, never waits), then updates its other tile-columns; the other warps `bar.sync`.
 //   * The trailing update runs on the FP64 tensor path: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); a complex 8x8x4
 //     product is 4 real DMMAs; C fragments are read/written in shared memory, two tiles interleaved.
-//   * B rides along as columns R..R+2 (forward elimination); back substitution runs from the U rows in shared
-//     memory (one warp per right-hand side, solution column in registers).
+//   * B rides along as columns R..R+2 (forward elimination); the factoring warp replaces U11 by its inverse right
+//     after publishing a panel, and the back substitution is a left-looking chain of 8x8 DMMA products.
 #include <cstdio>
 #include <cstdlib>
 
@@ -56,6 +56,34 @@ __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.ar
 #define PODP_LU_TRACE 0
 #endif
 
+// The inverse of the upper-triangular diagonal block U11 of a factored panel replaces U11 in place (its slots are
+// dead: the trailing updates use L11, L21 and U12 only).  Lane -> (block kb0 + 8 (lane / 8), column lane % 8), nblk
+// <= 4 blocks per call; column c comes from back substitution with 1/U_kk from sRinv; all loads precede all writes.
+template <int LDA>
+__device__ __forceinline__ void invert_diag(double2 *A, const double2 *sRinv, int kb0, int nblk, int lane) {
+  constexpr int NB = 8;
+  double2 x[NB];
+  const bool act = lane < NB * nblk;
+  const int kb = kb0 + NB * (lane >> 3), c = lane & 7;
+  if (act) {
+#pragma unroll
+    for (int j = NB - 1; j >= 0; --j) {
+      const double2 rj = sRinv[kb + j];
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = j + 1; t < NB; ++t) acc = cfma(A[(kb + j) * LDA + kb + t], x[t], acc);
+      x[j] = j == c ? rj : (j < c ? cmul(make_double2(-acc.x, -acc.y), rj) : make_double2(0.0, 0.0));
+    }
+  }
+  __syncwarp();
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j <= c) A[(kb + j) * LDA + kb + c] = x[j];
+  }
+  __syncwarp();
+}
+
 }  // namespace lublk
 
 // dev instrumentation: clock64 stamps of block 0 / group 0 for its first 4 frequencies (off by default)
@@ -71,6 +99,9 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
   using C = lublk::Cfg<R, W>;
   constexpr int NCP = C::NCP, NTC = C::NTC, LDA = C::LDA, MS = C::MS, NB = lublk::NB, NT = W * 32;
   constexpr int NPAN = R / NB;
+  // U11^{-1} in place right after each panel is published (in the factoring warp's slack) or, where that slack is
+  // too short (W = 1, and the two-warp R = 48 case, measured), for all blocks just before the back substitution
+  constexpr bool INV_EARLY = W > 1 && !(W == 2 && R == 48);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = wid / W, w = wid % W;
@@ -260,7 +291,10 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       asm volatile("cp.async.commit_group;" ::: "memory");
       const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
       const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
-      for (int e = gl; e < 8 * R; e += NT) {
+#pragma unroll
+      for (int q = 0; q < (8 * R + NT - 1) / NT; ++q) {
+        const int e = q * NT + gl;
+        if (e >= 8 * R) break;
         const int i = e >> 3, c = e & 7;
         double2 v = make_double2(0.0, 0.0);
         if (c < 3) {
@@ -297,7 +331,10 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       if (info == 0) factor_panel(0, info);
       if (lane == 0) sPiv[R] = info;
       __syncwarp();
-      if constexpr (W > 1) lublk::bar_arrive(bar0, NT);
+      if constexpr (W > 1) {
+        lublk::bar_arrive(bar0, NT);
+        if (INV_EARLY && info == 0) lublk::invert_diag<LDA>(A, sRinv, 0, 1, lane);  // off the critical chain
+      }
     }
     for (int b = 0; b < NPAN; ++b) {
       const int owner = b % W;
@@ -310,6 +347,7 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       info = sPiv[R];
       const bool next = b + 1 < NPAN;
       const int nowner = (b + 1) % W;
+      bool inv_next = false;
       if (info == 0 && next && w == nowner) {
         // lookahead: the owner of tile-column b+1 updates it, factors panel b+1 and publishes it
         update_tile_col(b, b + 1);
@@ -317,9 +355,13 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
         factor_panel(b + 1, inf2);
         if (lane == 0) sPiv[R] = inf2;
         __syncwarp();
+        inv_next = inf2 == 0;
       }
       if (next && w == nowner) {
-        if constexpr (W > 1) lublk::bar_arrive(bar0 + ((b + 1) & 1), NT);
+        if constexpr (W > 1) {
+          lublk::bar_arrive(bar0 + ((b + 1) & 1), NT);
+          if (INV_EARLY && inv_next) lublk::invert_diag<LDA>(A, sRinv, (b + 1) * NB, 1, lane);  // off the chain
+        }
       }
       LB_TR(17 + 4 * b);
       if (info == 0) {
@@ -334,59 +376,83 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
     info = sPiv[R];
     LB_TR(2);
-    // ---- back substitution U x = y, blocked (warp 0): the NPAN diagonal 8x8 blocks of U are inverted in parallel
-    //      (one lane per block column; the strictly upper part of each inverse is stored transposed in the dead
-    //      L11 slots), then NPAN block steps x_b = Dinv_b y_b, y_above -= U_above,b x_b (lanes over rows x rhs).
+    // ---- back substitution U x = y, blocked and left-looking on the FP64 tensor path (warp 0).  The inverses
+    //      Dinv_b of the diagonal blocks were formed in place of U11 by the factoring warps (INV_EARLY) or are formed
+    //      here; for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), x_b = Dinv_b y_b.
+    //      The right-hand-side tile (8 columns, 3 used) is the DMMA n dimension.
     double2 *Pw = a.Pws + (size_t)t * 3 * R;
+    if constexpr (!INV_EARLY) {
+      if (info == 0) {  // every warp inverts up to 4 diagonal blocks (warp w: blocks 4w ..), then one hand-off
+        for (int b0 = 4 * w; b0 < NPAN; b0 += 4 * W)
+          lublk::invert_diag<LDA>(A, sRinv, b0 * NB, NPAN - b0 < 4 ? NPAN - b0 : 4, lane);
+        if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT);
+      }
+    }
     if (w == 0) {
       if (info == 0) {
-        for (int task = lane; task < NPAN * 8; task += 32) {
-          const int kb = (task >> 3) * 8, c = task & 7;
-          double2 x[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) x[j] = make_double2(0.0, 0.0);
-#pragma unroll
-          for (int j = 7; j >= 0; --j) {
-            if (j == c) x[j] = sRinv[kb + j];
-            if (j < c) {
-              double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-              for (int tt = j + 1; tt < 8; ++tt)
-                if (tt <= c) acc = cfma(A[(kb + j) * LDA + kb + tt], x[tt], acc);
-              x[j] = cmul(make_double2(-acc.x, -acc.y), sRinv[kb + j]);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j < c) A[(kb + c) * LDA + kb + j] = x[j];  // Dinv[j][c] stored at (c, j)
-        }
-        __syncwarp();
+        const int arow = lane >> 2, acol = lane & 3;
+        const int bk = lane & 3, bcol = lane >> 2;
+        const int crow = lane >> 2, ccol = 2 * (lane & 3);
         for (int b = NPAN - 1; b >= 0; --b) {
           const int kb = b * 8;
-          double2 xb = make_double2(0.0, 0.0);
-          const int r = lane / 3, c = lane - 3 * (lane / 3);
-          if (lane < 24) {
-            xb = cmul(sRinv[kb + r], A[(kb + r) * LDA + R + c]);
+          double2 y0 = A[(kb + crow) * LDA + R + ccol], y1 = A[(kb + crow) * LDA + R + ccol + 1];
+          double cr0 = y0.x, cr1 = y1.x, ci0 = y0.y, ci1 = y1.y;
+          double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
 #pragma unroll
-            for (int tt = 1; tt < 8; ++tt)
-              if (tt > r) xb = cfma(A[(kb + tt) * LDA + kb + r], A[(kb + tt) * LDA + R + c], xb);
+          for (int d = 1; d < NPAN; ++d) {
+            const int bb = b + d;
+            if (bb >= NPAN) break;
+            const int kc = bb * 8;
+            const double2 a0 = A[(kb + arow) * LDA + kc + acol], a1 = A[(kb + arow) * LDA + kc + 4 + acol];
+            const double2 x0 = A[(kc + bk) * LDA + R + bcol], x1 = A[(kc + 4 + bk) * LDA + R + bcol];
+            if (d & 1) {
+              lublk::dmma(cr0, cr1, -a0.x, x0.x);
+              lublk::dmma(ci0, ci1, -a0.x, x0.y);
+              lublk::dmma(cr0, cr1, a0.y, x0.y);
+              lublk::dmma(ci0, ci1, -a0.y, x0.x);
+              lublk::dmma(cr0, cr1, -a1.x, x1.x);
+              lublk::dmma(ci0, ci1, -a1.x, x1.y);
+              lublk::dmma(cr0, cr1, a1.y, x1.y);
+              lublk::dmma(ci0, ci1, -a1.y, x1.x);
+            } else {
+              lublk::dmma(dr0, dr1, -a0.x, x0.x);
+              lublk::dmma(di0, di1, -a0.x, x0.y);
+              lublk::dmma(dr0, dr1, a0.y, x0.y);
+              lublk::dmma(di0, di1, -a0.y, x0.x);
+              lublk::dmma(dr0, dr1, -a1.x, x1.x);
+              lublk::dmma(di0, di1, -a1.x, x1.y);
+              lublk::dmma(dr0, dr1, a1.y, x1.y);
+              lublk::dmma(di0, di1, -a1.y, x1.x);
+            }
           }
           __syncwarp();
-          if (lane < 24) A[(kb + r) * LDA + R + c] = xb;
+          A[(kb + crow) * LDA + R + ccol] = make_double2(cr0 + dr0, ci0 + di0);
+          A[(kb + crow) * LDA + R + ccol + 1] = make_double2(cr1 + dr1, ci1 + di1);
           __syncwarp();
-          for (int task = lane; task < kb * 3; task += 32) {
-            const int i = task / 3, cc = task - 3 * i;
-            double2 acc = A[i * LDA + R + cc];
-#pragma unroll
-            for (int tt = 0; tt < 8; ++tt) acc = cfms(A[i * LDA + kb + tt], A[(kb + tt) * LDA + R + cc], acc);
-            A[i * LDA + R + cc] = acc;
-          }
+          // x_b = Dinv_b y_b (Dinv_b stored in place of U11)
+          const int m = arow, k0 = acol, k1 = acol + 4;
+          const double2 v0 = m <= k0 ? A[(kb + m) * LDA + kb + k0] : make_double2(0.0, 0.0);
+          const double2 v1 = m <= k1 ? A[(kb + m) * LDA + kb + k1] : make_double2(0.0, 0.0);
+          const double2 x0 = A[(kb + bk) * LDA + R + bcol], x1 = A[(kb + 4 + bk) * LDA + R + bcol];
+          double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+          lublk::dmma(er0, er1, v0.x, x0.x);
+          lublk::dmma(ei0, ei1, v0.x, x0.y);
+          lublk::dmma(er0, er1, -v0.y, x0.y);
+          lublk::dmma(ei0, ei1, v0.y, x0.x);
+          lublk::dmma(er0, er1, v1.x, x1.x);
+          lublk::dmma(ei0, ei1, v1.x, x1.y);
+          lublk::dmma(er0, er1, -v1.y, x1.y);
+          lublk::dmma(ei0, ei1, v1.y, x1.x);
+          __syncwarp();
+          A[(kb + crow) * LDA + R + ccol] = make_double2(er0, ei0);
+          A[(kb + crow) * LDA + R + ccol + 1] = make_double2(er1, ei1);
           __syncwarp();
         }
         for (int e = lane; e < 3 * R; e += 32) {
           const int c = e / R, i = e - c * R;
-          Pw[e] = A[i * LDA + R + c];
-          if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = A[i * LDA + R + c];
+          const double2 v = A[i * LDA + R + c];
+          Pw[e] = v;
+          if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = v;
         }
       } else {
         for (int e = lane; e < 3 * R; e += 32) Pw[e] = make_double2(nanv, nanv);
