@@ -32,12 +32,14 @@ namespace ludyn {
 
 constexpr int NB = 8;
 
-template <int R, int W>
+// RG: the right-hand-side tile and the pivot reciprocals live in a per-group L2-resident scratch instead of shared
+// memory, which lets one more group fit per SM where A alone is just small enough (r = 48: 6 instead of 5).
+template <int R, int W, bool RG = false>
 struct Cfg {
   static_assert(R % 8 == 0, "R must be a multiple of 8 (exact padding)");
   static constexpr int NPAN = R / NB;           // panels
-  static constexpr int NCP = R + 8;             // columns incl. the RHS tile (R..R+2 used)
-  static constexpr int NTC = NCP / 8;           // tile-columns (= NPAN + 1)
+  static constexpr int NCP = RG ? R : R + 8;    // shared-memory columns (+ the RHS tile R..R+7 unless RG)
+  static constexpr int NTC = NPAN + 1;          // tile-columns incl. the right-hand-side tile
   static constexpr int LDA = NCP + 1;           // row stride (complex), odd
   static constexpr int MS = (R + 31) / 32;      // panel row slots per lane
   static constexpr int NOWN = (NTC + W - 1) / W;  // tile-columns per warp (upper bound)
@@ -45,8 +47,8 @@ struct Cfg {
   // A, 1/U_kk (R), orig (R), dst (R), {published panels, info, pad}, pivot-row scratch (9)
   // ... + one mbarrier per panel (completes when the panel is published)
   // (rounded to 16 B so that every group's base stays aligned)
-  static constexpr int G_BYTES = (A_ELEMS * 16 + R * 16 + 2 * R * 4 + 16 + 9 * 16 + NPAN * 8 + 15) / 16 * 16;
-  static constexpr int GROUPS_SMEM = (225 * 1024) / G_BYTES;
+  static constexpr int G_BYTES = (A_ELEMS * 16 + (RG ? 0 : R * 16) + 2 * R * 4 + 16 + 9 * 16 + NPAN * 8 + 15) / 16 * 16;
+  static constexpr int GROUPS_SMEM = (227 * 1024) / G_BYTES;
   static constexpr int GROUPS_T = (16 / W) < 15 ? (16 / W) : 15;  // <= 16 warps, one named barrier per group
   static constexpr int GROUPS = GROUPS_SMEM < GROUPS_T ? GROUPS_SMEM : GROUPS_T;
   static constexpr int THREADS = GROUPS * W * 32;
@@ -269,8 +271,10 @@ __device__ __forceinline__ void invert_diag(double2 *A, const double2 *sRinv, in
 }
 
 // U: apply the panel at kb to the tile-column at col0 (NRT = row tiles below the panel, compile-time).
-template <int R, int LDA, int NRT>
-__device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, const int *sDst, int kb, int col0,
+// The tile-column is addressed through Ct (its column 0) with row stride LDC: Ct = A + col0, LDC = LDA for a
+// column in shared memory, or the group's L2-resident right-hand-side tile (LDC = 8) in the RG mode.
+template <int R, int LDA, int NRT, int LDC>
+__device__ __forceinline__ void update_tile_col(double2 *A, double2 *Ct, const int *sOrig, const int *sDst, int kb,
                                                 int lane) {
   constexpr int NB = 8;
   // (1) permutation in one pass and U12 = L11^{-1} (P A12) on DMMA: the B-fragments of P A12 are read straight
@@ -279,16 +283,16 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
     const int arow = lane >> 2, acol = lane & 3;
     const int bk = lane & 3, bcol = lane >> 2;
     const int crow = lane >> 2, ccol = 2 * (lane & 3);
-    const double2 x0 = A[sOrig[kb + bk] * LDA + col0 + bcol], x1 = A[sOrig[kb + 4 + bk] * LDA + col0 + bcol];
+    const double2 x0 = Ct[sOrig[kb + bk] * LDC + bcol], x1 = Ct[sOrig[kb + 4 + bk] * LDC + bcol];
     const int dst = sDst[kb + crow];
-    const double2 o0 = A[(kb + crow) * LDA + col0 + ccol], o1 = A[(kb + crow) * LDA + col0 + ccol + 1];
+    const double2 o0 = Ct[(kb + crow) * LDC + ccol], o1 = Ct[(kb + crow) * LDC + ccol + 1];
     const double2 one = make_double2(1.0, 0.0), zero = make_double2(0.0, 0.0);
     const double2 v0 = arow > acol ? A[(kb + arow) * LDA + kb + acol] : (arow == acol ? one : zero);
     const double2 v1 = arow > acol + 4 ? A[(kb + arow) * LDA + kb + acol + 4] : (arow == acol + 4 ? one : zero);
     __syncwarp();
     if (dst >= kb + NB) {
-      A[dst * LDA + col0 + ccol] = o0;
-      A[dst * LDA + col0 + ccol + 1] = o1;
+      Ct[dst * LDC + ccol] = o0;
+      Ct[dst * LDC + ccol + 1] = o1;
     }
     double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
     dmma(er0, er1, v0.x, x0.x);
@@ -299,8 +303,8 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
     dmma(ei0, ei1, v1.x, x1.y);
     dmma(er0, er1, -v1.y, x1.y);
     dmma(ei0, ei1, v1.y, x1.x);
-    A[(kb + crow) * LDA + col0 + ccol] = make_double2(er0, ei0);
-    A[(kb + crow) * LDA + col0 + ccol + 1] = make_double2(er1, ei1);
+    Ct[(kb + crow) * LDC + ccol] = make_double2(er0, ei0);
+    Ct[(kb + crow) * LDC + ccol + 1] = make_double2(er1, ei1);
   }
   __syncwarp();
   if constexpr (NRT > 0) {
@@ -309,7 +313,7 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
     const int arow = lane >> 2, acol = lane & 3;
     const int bk = lane & 3, bcol = lane >> 2;
     const int crow = lane >> 2, ccol = 2 * (lane & 3);
-    const double2 b0 = A[(kb + bk) * LDA + col0 + bcol], b1 = A[(kb + 4 + bk) * LDA + col0 + bcol];
+    const double2 b0 = Ct[(kb + bk) * LDC + bcol], b1 = Ct[(kb + 4 + bk) * LDC + bcol];
 #pragma unroll
     for (int t0 = 0; t0 < NRT; t0 += CH) {
       double2 a0[CH], a1[CH], c0[CH], c1[CH];
@@ -319,8 +323,8 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
           const int tr = kb + NB + 8 * (t0 + q);
           a0[q] = A[(tr + arow) * LDA + kb + acol];
           a1[q] = A[(tr + arow) * LDA + kb + 4 + acol];
-          c0[q] = A[(tr + crow) * LDA + col0 + ccol];
-          c1[q] = A[(tr + crow) * LDA + col0 + ccol + 1];
+          c0[q] = Ct[(tr + crow) * LDC + ccol];
+          c1[q] = Ct[(tr + crow) * LDC + ccol + 1];
         }
       }
 #pragma unroll
@@ -344,8 +348,8 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
       for (int q = 0; q < CH; ++q) {
         if (t0 + q < NRT) {
           const int tr = kb + NB + 8 * (t0 + q);
-          A[(tr + crow) * LDA + col0 + ccol] = c0[q];
-          A[(tr + crow) * LDA + col0 + ccol + 1] = c1[q];
+          Ct[(tr + crow) * LDC + ccol] = c0[q];
+          Ct[(tr + crow) * LDC + ccol + 1] = c1[q];
         }
       }
     }
@@ -353,22 +357,38 @@ __device__ __forceinline__ void update_tile_col(double2 *A, const int *sOrig, co
   __syncwarp();
 }
 
-template <int R, int LDA, int N = R / 8 - 1>
-__device__ __forceinline__ void update_dispatch(double2 *A, const int *sOrig, const int *sDst, int b, int col0,
+template <int R, int LDA, int LDC, int N = R / 8 - 1>
+__device__ __forceinline__ void update_dispatch(double2 *A, double2 *Ct, const int *sOrig, const int *sDst, int b,
                                                 int lane) {
   // NRT = R/8 - 1 - b: one instantiation per panel index keeps every loop bound and offset compile-time
   if (R / 8 - 1 - b == N) {
-    update_tile_col<R, LDA, N>(A, sOrig, sDst, b * 8, col0, lane);
+    update_tile_col<R, LDA, N, LDC>(A, Ct, sOrig, sDst, b * 8, lane);
   } else if constexpr (N > 0) {
-    update_dispatch<R, LDA, N - 1>(A, sOrig, sDst, b, col0, lane);
+    update_dispatch<R, LDA, LDC, N - 1>(A, Ct, sOrig, sDst, b, lane);
   }
+}
+
+// C -> B re-layout of an 8x8 complex tile by shuffles (C: lane holds row lane/4, columns 2(lane%4), +1; B: lane holds
+// rows lane%4 and lane%4 + 4 of column lane/4).
+__device__ __forceinline__ void c_to_b(double2 c0, double2 c1, int lane, double2 &b0, double2 &b1) {
+  const unsigned FULL = 0xffffffffu;
+  const bool odd = (lane >> 2) & 1;
+  const int s0 = 4 * (lane & 3) + (lane >> 3), s1 = s0 + 16;
+  double2 u0, u1, w0, w1;
+  u0 = shfl2(c0, s0);
+  u1 = shfl2(c1, s0);
+  w0 = shfl2(c0, s1);
+  w1 = shfl2(c1, s1);
+  (void)FULL;
+  b0 = odd ? u1 : u0;
+  b1 = odd ? w1 : w0;
 }
 
 }  // namespace ludyn
 
-template <int R, int W>
-__global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(EvalArgs a) {
-  using C = ludyn::Cfg<R, W>;
+template <int R, int W, bool RG>
+__global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kernel(EvalArgs a) {
+  using C = ludyn::Cfg<R, W, RG>;
   constexpr int NTC = C::NTC, LDA = C::LDA, MS = C::MS, NB = ludyn::NB, NT = W * 32, NPAN = C::NPAN;
   constexpr int NOWN = C::NOWN;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -376,8 +396,10 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
   const int grp = wid / W, w = wid % W;
   unsigned char *gbase = smem_raw + (size_t)grp * C::G_BYTES;
   double2 *A = reinterpret_cast<double2 *>(gbase);
-  double2 *sRinv = A + C::A_ELEMS;
-  int *sOrig = reinterpret_cast<int *>(sRinv + R);  // sOrig[q]: pre-step position of the row now at q (q in panel)
+  // RG: per-group scratch in L2: RHS tile (R x 8, row stride 8) then 1/U_kk (R)
+  double2 *gRHS = RG ? a.gscr + ((size_t)blockIdx.x * C::GROUPS + grp) * (9 * R) : nullptr;
+  double2 *sRinv = RG ? gRHS + 8 * R : A + C::A_ELEMS;
+  int *sOrig = reinterpret_cast<int *>(A + C::A_ELEMS + (RG ? 0 : R));  // pre-step position of the row now at q
   int *sDst = sOrig + R;                             // sDst[o]: final position of the row that was at o (o in panel)
   int *sPub = sDst + R;                              // [0] panels published, [1] info
   double2 *sRow = reinterpret_cast<double2 *>(sPub + 4);  // pivot-row scratch (8 values + position)
@@ -433,7 +455,7 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
           const double2 x0 = __ldg(gb0 + c * R + i), x1 = __ldg(gb1 + c * R + i);
           v = make_double2(fma(om, x1.x, x0.x), fma(om, x1.y, x0.y));
         }
-        A[i * LDA + R + c] = v;
+        if constexpr (RG) gRHS[i * 8 + c] = v; else A[i * LDA + R + c] = v;
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -540,7 +562,11 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
         }
         {
           LD_TR_BEGIN();
-          ludyn::update_dispatch<R, LDA>(A, sOrig, sDst, ub, (w + uq * W) * 8, lane);
+          const int tcu = w + uq * W;
+          if (RG && tcu == NPAN)
+            ludyn::update_dispatch<R, LDA, 8>(A, gRHS, sOrig, sDst, ub, lane);
+          else
+            ludyn::update_dispatch<R, LDA, LDA>(A, A + tcu * 8, sOrig, sDst, ub, lane);
           LD_TR_END(2, ub, w + uq * W);
         }
 #pragma unroll
@@ -571,6 +597,73 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
         const int arow = lane >> 2, acol = lane & 3;
         const int bk = lane & 3, bcol = lane >> 2;
         const int crow = lane >> 2, ccol = 2 * (lane & 3);
+        if constexpr (RG) {
+          // y prefetched from the L2 scratch once; x kept as B fragments in registers (C -> B by shuffles); the
+          // solution goes straight from the C fragments to the hand-off workspace
+          double2 ya[NPAN], yb[NPAN], xb0[NPAN], xb1[NPAN];
+#pragma unroll
+          for (int b = 0; b < NPAN; ++b) {
+            ya[b] = gRHS[(8 * b + crow) * 8 + ccol];
+            yb[b] = gRHS[(8 * b + crow) * 8 + ccol + 1];
+          }
+#pragma unroll
+          for (int b = NPAN - 1; b >= 0; --b) {
+            const int kb = b * 8;
+            double cr0 = ya[b].x, cr1 = yb[b].x, ci0 = ya[b].y, ci1 = yb[b].y;
+            double dr0 = 0.0, dr1 = 0.0, di0 = 0.0, di1 = 0.0;
+#pragma unroll
+            for (int bb = b + 1; bb < NPAN; ++bb) {
+              const int kc = bb * 8;
+              const double2 a0 = A[(kb + arow) * LDA + kc + acol], a1 = A[(kb + arow) * LDA + kc + 4 + acol];
+              const double2 x0 = xb0[bb], x1 = xb1[bb];
+              if ((bb - b) & 1) {
+                ludyn::dmma(cr0, cr1, -a0.x, x0.x);
+                ludyn::dmma(ci0, ci1, -a0.x, x0.y);
+                ludyn::dmma(cr0, cr1, a0.y, x0.y);
+                ludyn::dmma(ci0, ci1, -a0.y, x0.x);
+                ludyn::dmma(cr0, cr1, -a1.x, x1.x);
+                ludyn::dmma(ci0, ci1, -a1.x, x1.y);
+                ludyn::dmma(cr0, cr1, a1.y, x1.y);
+                ludyn::dmma(ci0, ci1, -a1.y, x1.x);
+              } else {
+                ludyn::dmma(dr0, dr1, -a0.x, x0.x);
+                ludyn::dmma(di0, di1, -a0.x, x0.y);
+                ludyn::dmma(dr0, dr1, a0.y, x0.y);
+                ludyn::dmma(di0, di1, -a0.y, x0.x);
+                ludyn::dmma(dr0, dr1, -a1.x, x1.x);
+                ludyn::dmma(di0, di1, -a1.x, x1.y);
+                ludyn::dmma(dr0, dr1, a1.y, x1.y);
+                ludyn::dmma(di0, di1, -a1.y, x1.x);
+              }
+            }
+            double2 y0b, y1b;
+            ludyn::c_to_b(make_double2(cr0 + dr0, ci0 + di0), make_double2(cr1 + dr1, ci1 + di1), lane, y0b, y1b);
+            const int m = arow, k0 = acol, k1 = acol + 4;
+            const double2 v0 = m <= k0 ? A[(kb + m) * LDA + kb + k0] : make_double2(0.0, 0.0);
+            const double2 v1 = m <= k1 ? A[(kb + m) * LDA + kb + k1] : make_double2(0.0, 0.0);
+            double er0 = 0.0, er1 = 0.0, ei0 = 0.0, ei1 = 0.0;
+            ludyn::dmma(er0, er1, v0.x, y0b.x);
+            ludyn::dmma(ei0, ei1, v0.x, y0b.y);
+            ludyn::dmma(er0, er1, -v0.y, y0b.y);
+            ludyn::dmma(ei0, ei1, v0.y, y0b.x);
+            ludyn::dmma(er0, er1, v1.x, y1b.x);
+            ludyn::dmma(ei0, ei1, v1.x, y1b.y);
+            ludyn::dmma(er0, er1, -v1.y, y1b.y);
+            ludyn::dmma(ei0, ei1, v1.y, y1b.x);
+            if (b > 0) ludyn::c_to_b(make_double2(er0, ei0), make_double2(er1, ei1), lane, xb0[b], xb1[b]);
+            const int row = kb + crow;
+            if (ccol < 3) {
+              Pw[ccol * R + row] = make_double2(er0, ei0);
+              if (a.P_out && row < a.r)
+                reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + ccol) * a.r + row] = make_double2(er0, ei0);
+            }
+            if (ccol + 1 < 3) {
+              Pw[(ccol + 1) * R + row] = make_double2(er1, ei1);
+              if (a.P_out && row < a.r)
+                reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + ccol + 1) * a.r + row] = make_double2(er1, ei1);
+            }
+          }
+        } else {
         for (int b = NPAN - 1; b >= 0; --b) {
           const int kb = b * 8;
           double2 y0 = A[(kb + crow) * LDA + R + ccol], y1 = A[(kb + crow) * LDA + R + ccol + 1];
@@ -635,6 +728,7 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
           Pw[e] = v;
           if (a.P_out && i < a.r) reinterpret_cast<double2 *>(a.P_out)[((size_t)t * 3 + c) * a.r + i] = v;
         }
+        }  // !RG
       } else {
         for (int e = lane; e < 3 * R; e += 32) Pw[e] = make_double2(nanv, nanv);
         if (a.P_out)
@@ -651,10 +745,24 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W>::THREADS, 1) lu_dyn_kernel(Ev
   }
 }
 
+template <int R, int W, bool RG>
+static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s);
+
 template <int R, int W>
 static cudaError_t launch_lu_dyn_t(const EvalArgs &a, cudaStream_t s) {
-  using C = ludyn::Cfg<R, W>;
-  auto kern = lu_dyn_kernel<R, W>;
+  // RG (right-hand sides in L2) only where it buys a group per SM and the scratch exists
+  constexpr bool RG = ludyn::Cfg<R, W, true>::GROUPS > ludyn::Cfg<R, W, false>::GROUPS;
+  const char *rg = getenv("PODP_LU_RG");  // dev switch: 0 = keep the right-hand sides in shared memory
+  if constexpr (RG) {
+    if (a.gscr && !(rg && rg[0] == '0')) return launch_lu_dyn_k<R, W, true>(a, s);
+  }
+  return launch_lu_dyn_k<R, W, false>(a, s);
+}
+
+template <int R, int W, bool RG>
+static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s) {
+  using C = ludyn::Cfg<R, W, RG>;
+  auto kern = lu_dyn_kernel<R, W, RG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -677,10 +785,10 @@ static cudaError_t launch_lu_dyn_t(const EvalArgs &a, cudaStream_t s) {
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
   const char *v = getenv("PODP_LU_W");
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, four at R = 56,
-  // 64 and 72..96
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48 and 56 (R = 56
+  // with the right-hand sides in L2: 4 groups per SM instead of 3), four at R = 64 and 72..96
   const int R = a.L.R;
-  const int wv = v ? atoi(v) : (R <= 40 ? 1 : (R == 48 ? 2 : 4));
+  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56) ? 2 : 4));
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \

@@ -491,6 +491,14 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
   cudaError_t e = cudaMallocFromPoolAsync((void **)&a.Pws, ws, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
+  a.gscr = nullptr;
+  if (!(flags & PODP_FLAG_PENCIL)) {  // per-group L2 scratch of the dynamically scheduled LU (right-hand sides)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const size_t gsz = (size_t)sms * 16 * 9 * c->L.R * sizeof(double2);
+    e = cudaMallocFromPoolAsync((void **)&a.gscr, gsz, c->pool, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(LU scratch)");
+  }
   int nl = 0;
   // N3 without the debug P output: solve for y only and run the MPT/certificate kernel in pencil coordinates
   const bool pencil_y = (flags & PODP_FLAG_PENCIL) && !(flags & PODP_FLAG_OUT_P) && !getenv("PODP_PENCIL_P");
@@ -545,6 +553,7 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
     }
   }
   cudaFreeAsync(a.Pws, s);
+  if (a.gscr) cudaFreeAsync(a.gscr, s);
   g_last_launches = nl;
   if (a.trace && getenv("PODP_LU_IMPL") && getenv("PODP_LU_IMPL")[0] == 'd') {  // lu_dyn task records (dev)
     cudaDeviceSynchronize();

@@ -39,6 +39,7 @@ struct EvalArgs {
   int32_t *info;
   double *P_out;       // debug P (nullable)
   double2 *Pws;        // workspace: n_obj x F x 3 x R complex (solve -> contraction hand-off)
+  double2 *gscr;       // LU scratch: 16 x SMs groups x 9 R complex (right-hand-side tile + 1/U_kk per group), nullable
   int flags;
   long long *trace;    // dev instrumentation (nullable): clock64 stamps of block 0 / group 0
 };
