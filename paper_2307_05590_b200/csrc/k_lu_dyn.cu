@@ -142,25 +142,14 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
     ++it_;
     ntr_ = 0;
     LD_TR_BEGIN();
-    // ---- a2: assemble [A | B | 0] (all W warps).  K is copied into A by cp.async (16 B per element, all copies in
-    //      flight at once, no registers); M is streamed through registers in two batches meanwhile; each thread
-    //      then adds i s M to the K entries it copied itself (cp.async.wait_all orders its own copies). ------------
+    // ---- a2: assemble [A | B | 0] (all W warps).  K and M stream through registers in batches (all loads of a
+    //      batch in flight at once) and A = K + i s M is written to shared memory once. -----------------------------
     {
       const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
       const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
       constexpr int PER = (R * R + NT - 1) / NT;
-      constexpr int HALF = (PER + 1) / 2;
+      constexpr int BAT = PER < 12 ? PER : 12;  // elements per batch and thread
       const int gl = w * 32 + lane;
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int e = q * NT + gl;
-        if (e < R * R) {
-          const int i = e / R, j = e - i * R;
-          const unsigned dst = (unsigned)__cvta_generic_to_shared(A + i * LDA + j);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gK + e) : "memory");
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
       const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
       const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
 #pragma unroll
@@ -176,21 +165,22 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
         if constexpr (RG) gRHS[i * 8 + c] = v; else A[i * LDA + R + c] = v;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double2 mm[HALF];
+      for (int q0 = 0; q0 < PER; q0 += BAT) {
+        double2 kk[BAT], mm[BAT];
 #pragma unroll
-        for (int q = 0; q < HALF; ++q) {
-          const int e = (h * HALF + q) * NT + gl;
-          if (h * HALF + q < PER && e < R * R) mm[q] = __ldg(gM + e);
+        for (int q = 0; q < BAT; ++q) {
+          const int e = (q0 + q) * NT + gl;
+          if (q0 + q < PER && e < R * R) {
+            kk[q] = __ldg(gK + e);
+            mm[q] = __ldg(gM + e);
+          }
         }
-        if (h == 0) asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-        for (int q = 0; q < HALF; ++q) {
-          const int e = (h * HALF + q) * NT + gl;
-          if (h * HALF + q < PER && e < R * R) {
+        for (int q = 0; q < BAT; ++q) {
+          const int e = (q0 + q) * NT + gl;
+          if (q0 + q < PER && e < R * R) {
             const int i = e / R, j = e - i * R;
-            const double2 kk = A[i * LDA + j];
-            A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk.x), fma(s, mm[q].x, kk.y));
+            A[i * LDA + j] = make_double2(fma(-s, mm[q].y, kk[q].x), fma(s, mm[q].x, kk[q].y));
           }
         }
       }
@@ -503,10 +493,10 @@ static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s) {
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
   const char *v = getenv("PODP_LU_W");
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48 and 56 (R = 56
-  // with the right-hand sides in L2: 4 groups per SM instead of 3), four at R = 64 and 72..96
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56 and 72 (R = 56
+  // with the right-hand sides in L2: 4 groups per SM instead of 3), four at R = 64 and 80..96
   const int R = a.L.R;
-  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56) ? 2 : 4));
+  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72) ? 2 : 4));
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \
