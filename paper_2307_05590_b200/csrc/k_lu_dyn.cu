@@ -493,10 +493,11 @@ static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s) {
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
   const char *v = getenv("PODP_LU_W");
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56 and 72 (R = 56
-  // with the right-hand sides in L2: 4 groups per SM instead of 3), four at R = 64 and 80..96
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80
+  // (R = 56 and 80 with the right-hand sides in L2: 4 instead of 3, 2 instead of 1 groups per SM), four at R = 64,
+  // 88 and 96
   const int R = a.L.R;
-  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72) ? 2 : 4));
+  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4));
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \
