@@ -159,12 +159,15 @@ def test_edge_cases_fast_path(torch_cuda, r):
     assert list(res["info"][0]) == [6, 6]
 
 
-@pytest.mark.parametrize("impl", ["b", "d"])
-@pytest.mark.parametrize("r", [8, 24, 40, 48, 72, 96])
+@pytest.mark.parametrize("impl", ["b", "d", "d-shared-rhs"])
+@pytest.mark.parametrize("r", [8, 24, 40, 48, 56, 72, 80, 96])
 def test_both_lu_kernels_parity_and_singular(torch_cuda, monkeypatch, impl, r):
     """Both LU kernels (lock-step blocked 'b', dynamically scheduled 'd'; the default picks one per padded R) stay
-    parity-green on every size class, including a zero pivot at a later panel (LAPACK info = k+1)."""
-    monkeypatch.setenv("PODP_LU_IMPL", impl)
+    parity-green on every size class, including a zero pivot at a later panel (LAPACK info = k+1).  At r = 48, 56 and
+    80 the dynamic kernel keeps the right-hand sides in L2 (RG mode); 'd-shared-rhs' forces them into shared memory."""
+    monkeypatch.setenv("PODP_LU_IMPL", impl[0])
+    if impl == "d-shared-rhs":
+        monkeypatch.setenv("PODP_LU_RG", "0")
     ops = g.make_operators(r, seed=r + 1)
     omega = np.r_[g.omega_grid(61), [np.inf]]
     res = run_gpu(torch_cuda, ops, omega)
