@@ -57,11 +57,19 @@ enum {
   PODP_FLAG_OUT_P = 1u << 1,    /* debug: also write P (n_obj x F x 3 x r complex, row-major) to P_d       */
   PODP_FLAG_NO_PIVOT = 1u << 2, /* LU without pivoting (exists since Re x^H A x = x^H K x > 0 for K > 0;
                                    SURVEY Appendix A.4).  Default is partial pivoting.                       */
-  PODP_FLAG_PENCIL = 1u << 3    /* NEXT row N3: solve with the pencil reduction precomputed by
+  PODP_FLAG_PENCIL = 1u << 3,   /* NEXT row N3: solve with the pencil reduction precomputed by
                                    podp_create (K = L L^H, L^{-1} M L^{-H} = V Lambda V^H, Z = L^{-H} V), i.e.
                                    P = Z (I + i omega nu Lambda)^{-1} Z^H B(omega): O(r^2) per frequency instead of
                                    the LU's O(r^3).  Exact in exact arithmetic; requires K positive definite
-                                   (PODP_ERR_UNSUPPORTED otherwise).  R, I, Delta are then formed as usual. */
+                                   (PODP_ERR_UNSUPPORTED otherwise).  R, I, Delta are then formed as usual.
+                                   The precompute runs once, on the first evaluation that asks for it.        */
+  /* Solver selection, for A/B measurement (at most one; none = the measured default: PODP_FLAG_LU_LL for padded
+     r <= 64, PODP_FLAG_LU_BLK / _DYN up to 96, PODP_FLAG_LU_GENERIC above).  Every choice computes the same
+     pivoted LU solve of P:593-596 up to rounding; a choice not instantiated for this r -> PODP_ERR_UNSUPPORTED. */
+  PODP_FLAG_LU_LL = 1u << 8,      /* left-looking block LU, one warp per frequency, padded r <= 64 (k_lu_ll.cu) */
+  PODP_FLAG_LU_BLK = 1u << 9,     /* lock-step panel-blocked LU, W warps per frequency, padded r <= 96        */
+  PODP_FLAG_LU_DYN = 1u << 10,    /* dynamically scheduled blocked LU, W warps per frequency, padded r <= 96  */
+  PODP_FLAG_LU_GENERIC = 1u << 11 /* generic one-warp LU (any r <= 128, pivoting or PODP_FLAG_NO_PIVOT)       */
 };
 
 /* Operators of ONE object (host pointers; copied, validated and packed by podp_create; caller keeps ownership).

@@ -52,10 +52,6 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-#ifndef PODP_LU_TRACE
-#define PODP_LU_TRACE 0
-#endif
-
 // The inverse of the upper-triangular diagonal block U11 of a factored panel replaces U11 in place (its slots are
 // dead: the trailing updates use L11, L21 and U12 only).  Lane -> (block kb0 + 8 (lane / 8), column lane % 8), nblk
 // <= 4 blocks per call; column c comes from back substitution with 1/U_kk from sRinv; all loads precede all writes.
@@ -86,14 +82,6 @@ __device__ __forceinline__ void invert_diag(double2 *A, const double2 *sRinv, in
 
 }  // namespace lublk
 
-// dev instrumentation: clock64 stamps of block 0 / group 0 for its first 4 frequencies (off by default)
-#define LB_TR(slot)                                                                                \
-  do {                                                                                             \
-    if constexpr (PODP_LU_TRACE)                                                                   \
-      if (a.trace && blockIdx.x == 0 && grp == 0 && w == 0 && lane == 0 && it_ < 4)              \
-        a.trace[it_ * 1024 + (slot)] = clock64();                                                 \
-  } while (0)
-
 template <int R, int W>
 __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(EvalArgs a) {
   using C = lublk::Cfg<R, W>;
@@ -115,8 +103,6 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
   const unsigned FULL = 0xffffffffu;
   const int ngroups_total = gridDim.x * C::GROUPS;
-  int it_ = -1;
-  (void)it_;
   (void)NCP;
 
   // ---- panel factorisation of tile-column b by the calling warp (sets info != 0 on a zero pivot) -------------
@@ -263,13 +249,11 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
   };
 
   for (int64_t t = (int64_t)blockIdx.x * C::GROUPS + grp; t < total; t += ngroups_total) {
-    ++it_;
     const int obj = (int)(t / a.F);
     const int64_t f = t - (int64_t)obj * a.F;
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
-    LB_TR(0);
     // ---- a2: assemble [A | B | 0] (all W warps).  K and M stream through registers in batches (all loads of a
     //      batch in flight at once) and A = K + i s M is written to shared memory once (one pass of shared-memory
     //      traffic per element instead of the copy + read-modify-write of a cp.async assembly). -----------------
@@ -315,7 +299,6 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       }
     }
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
-    LB_TR(1);
     int info = isfinite(om) ? 0 : -1;
     // ---- a3: blocked LU -- panel 0 by its owner (warp 0); group status lives in sPiv[R] ---------------------------
     if (w == 0) {
@@ -334,7 +317,6 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       } else {
         __syncwarp();
       }
-      LB_TR(16 + 4 * b);
       info = sPiv[R];
       const bool next = b + 1 < NPAN;
       const int nowner = (b + 1) % W;
@@ -354,7 +336,6 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
           if (INV_EARLY && inv_next) lublk::invert_diag<LDA>(A, sRinv, (b + 1) * NB, 1, lane);  // off the chain
         }
       }
-      LB_TR(17 + 4 * b);
       if (info == 0) {
         for (int tc = b + 1; tc < NTC; ++tc) {
           if (tc % W != w) continue;
@@ -362,11 +343,9 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
           update_tile_col(b, tc);
         }
       }
-      LB_TR(18 + 4 * b);
     }
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
     info = sPiv[R];
-    LB_TR(2);
     // ---- back substitution U x = y, blocked and left-looking on the FP64 tensor path (warp 0).  The inverses
     //      Dinv_b of the diagonal blocks were formed in place of U11 by the factoring warps (INV_EARLY) or are formed
     //      here; for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), x_b = Dinv_b y_b.
@@ -452,7 +431,6 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
             reinterpret_cast<double2 *>(a.P_out)[(size_t)t * 3 * a.r + e] = make_double2(nanv, nanv);
       }
     }
-    LB_TR(3);
     if (a.info && w == 0 && lane == 0) a.info[t] = info;
     if constexpr (W > 1) lublk::bar_sync(bar0 + 2, NT); else __syncwarp();
   }
@@ -471,22 +449,14 @@ static cudaError_t launch_lu_blk_t(const EvalArgs &a, cudaStream_t s) {
   int64_t blocks = (total + C::GROUPS - 1) / C::GROUPS;
   if (blocks > sms) blocks = sms;
   kern<<<(unsigned)blocks, C::THREADS, C::BYTES, s>>>(a);
-  cudaError_t le = cudaGetLastError();
-  if (le != cudaSuccess && getenv("PODP_LU_DEBUG")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "lu_blk<%d,%d>: threads %d bytes %zu regs %d maxThreads %d local %zu static_smem %zu\n", R, W,
-            C::THREADS, C::BYTES, fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes);
-  }
-  return le;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
-  const char *v = getenv("PODP_LU_W");
   // measured on B200 (tools/r_sweep.py): one warp per frequency is best for r <= 32, two for r = 40..56, four for
   // r = 64..72, eight for r >= 80 (shared memory then holds a single frequency per SM)
-  const int wv = v ? atoi(v) : (a.L.R >= 80 ? 8 : (a.L.R >= 64 ? 4 : (a.L.R >= 40 ? 2 : 1)));
+  const int wv = (a.L.R >= 80 ? 8 : (a.L.R >= 64 ? 4 : (a.L.R >= 40 ? 2 : 1)));
   switch (a.L.R) {
 #define PODP_CASE(RR)                                 \
   case RR:                                            \

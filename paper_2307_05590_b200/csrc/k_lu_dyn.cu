@@ -82,25 +82,7 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 __device__ __forceinline__ void st_release(int *p, int v) {
   asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
-#ifndef PODP_LU_TRACE
-#define PODP_LU_TRACE 0
-#endif
-
 }  // namespace ludyn
-
-// dev instrumentation (build with -DPODP_LU_TRACE=1, run with PODP_LU_TRACE=1): per-task clock64 records of block 0,
-// group 0, frequencies 1 and 2 -- trace[(it-1)*2048 + w*256 + 3k + {0,1,2}] = {kind<<16 | b<<8 | tile, start, end}
-#define LD_TR_BEGIN() const long long tr_t0_ = PODP_LU_TRACE ? clock64() : 0
-#define LD_TR_END(kind, b, tc)                                                                                   \
-  do {                                                                                                           \
-    if constexpr (PODP_LU_TRACE)                                                                                 \
-      if (a.trace && blockIdx.x == 0 && grp == 0 && lane == 0 && (it_ == 0 || it_ == 1) && ntr_ < 80) {       \
-        long long *tp = a.trace + it_ * 2048 + w * 256 + 3 * ntr_++;                                      \
-        tp[0] = ((kind) << 16) | ((b) << 8) | (tc);                                                              \
-        tp[1] = tr_t0_;                                                                                          \
-        tp[2] = clock64();                                                                                       \
-      }                                                                                                          \
-  } while (0)
 
 
 
@@ -130,8 +112,6 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
   const int64_t total = (int64_t)a.n_obj * a.F;
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
   const int ngroups_total = gridDim.x * C::GROUPS;
-  int it_ = -1, ntr_ = 0;
-  (void)ntr_;
 
   for (int64_t t = (int64_t)blockIdx.x * C::GROUPS + grp; t < total; t += ngroups_total) {
     const int obj = (int)(t / a.F);
@@ -139,9 +119,6 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
-    ++it_;
-    ntr_ = 0;
-    LD_TR_BEGIN();
     // ---- a2: assemble [A | B | 0] (all W warps).  K and M stream through registers in batches (all loads of a
     //      batch in flight at once) and A = K + i s M is written to shared memory once. -----------------------------
     {
@@ -190,9 +167,10 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
       }
     }
     if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
-    LD_TR_END(0, 0, 0);
     // ---- a3: dynamically scheduled blocked LU ------------------------------------------------------------------------
-    const bool lu_run = sPub[1] == 0;
+    // every warp derives the LU's go/no-go from omega itself: sPub[1] may already carry a zero-pivot info written
+    // by a warp that started factoring (data race on the shared status word)
+    const bool lu_run = isfinite(om);
     if (lu_run) {
       int done[NOWN];  // updates applied to each owned tile-column (tile w + q W)
 #pragma unroll
@@ -213,13 +191,9 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
               qn = q;
             }
           if (dn == nf) {
-            LD_TR_BEGIN();
-            long long *ftr = (PODP_LU_TRACE && a.trace && blockIdx.x == 0 && grp == 0 && (it_ == 0 || it_ == 1))
-                                 ? a.trace + 4096 + it_ * 1024 + nf * 32
-                                 : nullptr;
             const int inf = (R - nf * NB > 32)
-                                ? ludyn::factor_panel<R, LDA, MS>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane, ftr)
-                                : ludyn::factor_panel<R, LDA, 1>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane, ftr);
+                                ? ludyn::factor_panel<R, LDA, MS>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane)
+                                : ludyn::factor_panel<R, LDA, 1>(A, sRinv, sOrig, sDst, sRow, nf * NB, lane);
             __threadfence_block();
             __syncwarp();
             if (lane == 0) {
@@ -227,7 +201,6 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
               ludyn::st_release(sPub, nf + 1);
               ludyn::mbar_arrive(sBar + nf);
             }
-            LD_TR_END(1, nf, nf);
             if (nf + 1 > pub) pub = nf + 1;
             // W > 1: invert U11 now, in the slack before this warp's next critical task; W = 1 does all blocks at the end
             if constexpr (W > 1)
@@ -269,13 +242,11 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
           ub = best_d;
         }
         {
-          LD_TR_BEGIN();
           const int tcu = w + uq * W;
           if (RG && tcu == NPAN)
             ludyn::update_dispatch<R, LDA, 8>(A, gRHS, sOrig, sDst, ub, lane);
           else
             ludyn::update_dispatch<R, LDA, LDA>(A, A + tcu * 8, sOrig, sDst, ub, lane);
-          LD_TR_END(2, ub, w + uq * W);
         }
 #pragma unroll
         for (int q = 0; q < NOWN; ++q)
@@ -283,13 +254,10 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
       }
     }
     {
-      LD_TR_BEGIN();
       if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
-      LD_TR_END(3, 0, 0);
     }
     if (lu_run) lu_par ^= 1u;
     const int info = sPub[1];
-    const long long tr_bs_ = PODP_LU_TRACE ? clock64() : 0;
     // ---- back substitution U x = y, blocked and left-looking on the FP64 tensor path.
     //      The inverses Dinv_b of the diagonal blocks were formed in place by the factoring warps (invert_diag);
     //      warp 0, for b = NPAN-1 .. 0: y_b -= sum_{b' > b} U_{b b'} x_{b'} (DMMA, two accumulators), then
@@ -444,10 +412,6 @@ __global__ void __launch_bounds__(ludyn::Cfg<R, W, RG>::THREADS, 1) lu_dyn_kerne
             reinterpret_cast<double2 *>(a.P_out)[(size_t)t * 3 * a.r + e] = make_double2(nanv, nanv);
       }
       if (a.info && lane == 0) a.info[t] = info;
-      {
-        const long long tr_t0_ = tr_bs_;
-        LD_TR_END(4, 0, 0);
-      }
     }
     if constexpr (W > 1) ludyn::bar_sync(bar_id, NT); else __syncwarp();
   }
@@ -460,9 +424,8 @@ template <int R, int W>
 static cudaError_t launch_lu_dyn_t(const EvalArgs &a, cudaStream_t s) {
   // RG (right-hand sides in L2) only where it buys a group per SM and the scratch exists
   constexpr bool RG = ludyn::Cfg<R, W, true>::GROUPS > ludyn::Cfg<R, W, false>::GROUPS;
-  const char *rg = getenv("PODP_LU_RG");  // dev switch: 0 = keep the right-hand sides in shared memory
   if constexpr (RG) {
-    if (a.gscr && !(rg && rg[0] == '0')) return launch_lu_dyn_k<R, W, true>(a, s);
+    if (a.gscr) return launch_lu_dyn_k<R, W, true>(a, s);
   }
   return launch_lu_dyn_k<R, W, false>(a, s);
 }
@@ -480,24 +443,18 @@ static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s) {
   int64_t blocks = (total + C::GROUPS - 1) / C::GROUPS;
   if (blocks > sms) blocks = sms;
   kern<<<(unsigned)blocks, C::THREADS, C::BYTES, s>>>(a);
-  cudaError_t le = cudaGetLastError();
-  if (le != cudaSuccess && getenv("PODP_LU_DEBUG")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "lu_dyn<%d,%d>: threads %d bytes %zu regs %d maxThreads %d local %zu\n", R, W, C::THREADS,
-            C::BYTES, fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes);
-  }
-  return le;
+  return cudaGetLastError();
 }
+
+size_t lu_dyn_scratch_bytes(int R, int sms) { return (size_t)sms * 16 * 9 * R * sizeof(double2); }
 
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
-  const char *v = getenv("PODP_LU_W");
   // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80
   // (R = 56 and 80 with the right-hand sides in L2: 4 instead of 3, 2 instead of 1 groups per SM), four at R = 64,
   // 88 and 96
   const int R = a.L.R;
-  const int wv = v ? atoi(v) : (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4));
+  const int wv = (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4));
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \

@@ -1,0 +1,505 @@
+// K2 default path (R <= 64): left-looking block LU with partial pivoting + 3-RHS solve, ONE WARP PER FREQUENCY
+// (rows a2-a3 of SURVEY 8(a)).
+//   A(omega) = K + i omega nu M,  B(omega) = b0 + omega b1,  P = A^{-1} B            (eqn:ReducedA)
+//
+// Factorisation (the same pivots and the same trailing updates as LAPACK's blocked getrf, reordered):
+//   P_perm A = Lhat Uhat,  Lhat = [I; M_tb] block unit lower (8x8 identity diagonal blocks),
+//   Uhat = [Y_tc (t < c); Uhat_cc = L_cc U_cc] block upper, where for 8-column panel c (rows 8c .. R-1, after the
+//   updates of panels 0..c-1) P_c [A_cc; A_tc] = [L_cc; L_tc] U_cc is an unblocked LU with partial pivoting,
+//   M_tc = L_tc L_cc^{-1}, and Y_tc = A_tc - sum_{b<t} M_tb Y_bc is block (t, c) of the right-looking getrf
+//   update before its L_tt^{-1} solve (U_tc = L_tt^{-1} Y_tc).  Then z = Lhat^{-1} P_perm B (forward, 3 columns)
+//   and x = Uhat^{-1} z (block back substitution with D_t = Uhat_tt^{-1}).
+//
+// Layout.  Column tile c (8 columns) is accumulated in REGISTERS as DMMA C fragments (acc_t, t = 0..NT-1):
+//   acc = A[perm rows, c] - sum_b M_{:,b} Y_{b,c} on mma.sync.m8n8k4.f64 (SASS DMMA; a complex 8x8x8 tile product is
+//   8 DMMA), so trailing-update results never round-trip through shared memory; only the M strips (M_{t,b}, read
+//   as A fragments, XOR-swizzled rows: conflict-free both as A fragments and as lane = row panel rows) live in the
+//   warp's shared-memory slice.  Y_{t,c} (t < c) and D_t go to a per-warp L2-resident scratch (read once by the
+//   back substitution).  The panel is factored in registers with lane = row (redux.sync argmax of an integer
+//   magnitude key, pivot-row broadcast through 9 complex of shared memory, speculative per-candidate reciprocals
+//   so the reciprocal is off the pivot chain).  Rows never move: a position -> physical-row map (perm) gathers K
+//   and M rows at assembly time and the M strips of earlier panels are re-ordered only when a panel interchanged
+//   rows.  The 3-column right-hand side is real-ified (8 x [Re | Im] columns): a complex 8x8 by 8x3 product is 4 DMMA.
+//   One warp owns one frequency end to end (no inter-warp synchronisation); G independent warps per CTA.
+#include <utility>
+
+#include "podp_common.cuh"
+
+namespace podp {
+
+namespace lull {
+
+template <int R>
+struct Cfg {
+  static_assert(R % 8 == 0 && R >= 8 && R <= 64, "left-looking kernel: R in 8..64, multiple of 8");
+  static constexpr int NT = R / 8;                       // tile rows / columns
+  static constexpr int STRIP_TILES = NT * (NT + 1) / 2;  // strip b holds tiles b..NT-1 (diag tile = L\U)
+  static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
+  static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16;
+  static constexpr int G_SMEM = (227 * 1024) / W_BYTES;
+  static constexpr int G = G_SMEM < 16 ? G_SMEM : 16;    // warps (= concurrent frequencies) per CTA
+  static constexpr int GSCR_TILES = NT * (NT + 1) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT
+  static constexpr size_t BYTES = (size_t)G * W_BYTES;
+  static_assert(G >= 1, "strips do not fit in shared memory");
+};
+
+// first tile of strip b
+__host__ __device__ constexpr int strip_off(int NT, int b) { return b * NT - b * (b - 1) / 2; }
+// row swizzle: slot = k ^ swz(i & 7) makes both lane = row reads (8 rows, same k) and A-fragment reads (rows 2j,
+// 2j+1 x 4 consecutive k) hit 8 distinct 16-byte bank groups
+__device__ __forceinline__ int swz(int i) { return ((i & 1) << 2) | ((i >> 1) & 3); }
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// IEEE-safe complex reciprocal for pivots whose |z|^2 is outside the fast path's normal range
+__device__ __noinline__ double2 crecip_slow(double2 z) {
+  const double m = fmax(fabs(z.x), fabs(z.y));
+  const double zx = z.x / m, zy = z.y / m;
+  const double inv = 1.0 / (fma(zx, zx, zy * zy) * m);
+  return make_double2(zx * inv, -zy * inv);
+}
+
+// B fragment (k = 4s + lane%4, n = lane/4) of an 8x8 tile held as C fragments (row lane/4, cols 2(lane%4) + {0,1})
+__device__ __forceinline__ double frag_c2b(double c0, double c1, int s, int lane) {
+  const int src = 16 * s + 4 * (lane & 3) + (lane >> 3);
+  const double v0 = __shfl_sync(0xffffffffu, c0, src), v1 = __shfl_sync(0xffffffffu, c1, src);
+  return ((lane >> 2) & 1) ? v1 : v0;
+}
+
+// Real-ified right-hand side tile Z = [Re z_0..2 | Im z_0..2 | 0 0] (C fragments) -> B fragments of Z (b1) and of
+// Z' = [-Im z | Re z | 0 0] (b2), so that a complex 8x8 A times z is  Re(A) Z + Im(A) Z'  (2 DMMA per k-step).
+__device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double (&b1)[2], double (&b2)[2]) {
+  const int n = lane >> 2;
+  const int j2 = n < 3 ? n + 3 : (n < 6 ? n - 3 : 6);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int row = 4 * (4 * s + (lane & 3));
+    const int src1 = row + (n >> 1), src2 = row + (j2 >> 1);
+    const double u0 = __shfl_sync(0xffffffffu, c0, src1), u1 = __shfl_sync(0xffffffffu, c1, src1);
+    const double w0 = __shfl_sync(0xffffffffu, c0, src2), w1 = __shfl_sync(0xffffffffu, c1, src2);
+    b1[s] = (n & 1) ? u1 : u0;
+    const double w = (j2 & 1) ? w1 : w0;
+    b2[s] = n < 3 ? -w : (n < 6 ? w : 0.0);
+  }
+}
+
+// Column c, block b: Y_{b,c} = acc_b is final -> scratch (C-fragment order) and acc_t -= M_{t,b} Y_{b,c}, t > b.
+template <int NT, int B>
+__device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S, double2 *gY,
+                                     int lane) {
+  gY[2 * lane] = make_double2(ar[B][0], ai[B][0]);
+  gY[2 * lane + 1] = make_double2(ar[B][1], ai[B][1]);
+  double nyr[2], yi[2], nyi[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const double r = frag_c2b(ar[B][0], ar[B][1], s, lane), i = frag_c2b(ai[B][0], ai[B][1], s, lane);
+    nyr[s] = -r;
+    yi[s] = i;
+    nyi[s] = -i;
+  }
+  const int r4 = lane >> 2, q = lane & 3;
+  const double2 *Sb = S + strip_off(NT, B) * 64;
+  const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
+#pragma unroll
+  for (int t = B + 1; t < NT; ++t) {
+    const double2 *row = Sb + (8 * (t - B) + r4) * 8;
+    const double2 m0 = row[k0], m1 = row[k1];
+    // acc -= M Y :  Re += Mr (-Yr) + Mi Yi ;  Im += Mr (-Yi) + Mi (-Yr)
+    dmma(ar[t][0], ar[t][1], m0.x, nyr[0]);
+    dmma(ai[t][0], ai[t][1], m0.x, nyi[0]);
+    dmma(ar[t][0], ar[t][1], m0.y, yi[0]);
+    dmma(ai[t][0], ai[t][1], m0.y, nyr[0]);
+    dmma(ar[t][0], ar[t][1], m1.x, nyr[1]);
+    dmma(ai[t][0], ai[t][1], m1.x, nyi[1]);
+    dmma(ar[t][0], ar[t][1], m1.y, yi[1]);
+    dmma(ai[t][0], ai[t][1], m1.y, nyr[1]);
+  }
+}
+
+template <int NT, int B = 0>
+__device__ __forceinline__ void body_dispatch(int b, double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S,
+                                              double2 *gY, int lane) {
+  if constexpr (B < NT - 1) {
+    if (b == B) body<NT, B>(ar, ai, S, gY, lane);
+    else body_dispatch<NT, B + 1>(b, ar, ai, S, gY, lane);
+  }
+}
+
+// Forward substitution z_t -= M_{t,B} z_B (real-ified right-hand side), t > B
+template <int NT, int B>
+__device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, int lane) {
+  double b1[2], b2[2];
+  rhs_frags(z[B][0], z[B][1], lane, b1, b2);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    b1[s] = -b1[s];
+    b2[s] = -b2[s];
+  }
+  const int r4 = lane >> 2, q = lane & 3;
+  const double2 *Sb = S + strip_off(NT, B) * 64;
+  const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
+#pragma unroll
+  for (int t = B + 1; t < NT; ++t) {
+    const double2 *row = Sb + (8 * (t - B) + r4) * 8;
+    const double2 m0 = row[k0], m1 = row[k1];
+    dmma(z[t][0], z[t][1], m0.x, b1[0]);
+    dmma(z[t][0], z[t][1], m0.y, b2[0]);
+    dmma(z[t][0], z[t][1], m1.x, b1[1]);
+    dmma(z[t][0], z[t][1], m1.y, b2[1]);
+  }
+}
+
+// A fragment (row lane/4, k = 4s + lane%4) of a complex tile stored in C-fragment order (element (i, k) at
+// 2 * (4 i + k / 2) + k % 2), from the L2 scratch
+__device__ __forceinline__ double2 afrag_cstore(const double2 *g, int s, int lane) {
+  const int k = 4 * s + (lane & 3);
+  return __ldcg(g + 2 * (4 * (lane >> 2) + (k >> 1)) + (k & 1));
+}
+
+// Unblocked LU with partial pivoting of panel c (rows 8c .. R-1 of strip c, lane = row), M_tc = L_tc L_cc^{-1},
+// interchanges applied to perm and to the strips of earlier panels.  Returns 0 or (LAPACK getrf info) k + 1 for
+// an exactly zero pivot column at global step k.
+template <int R, int MSE, bool PIVOT>
+__device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, int lane) {
+  constexpr int NT = R / 8;
+  const int kb = 8 * c;
+  double2 *St = S + strip_off(NT, c) * 64;
+  double2 pn[MSE][8];
+  int pos[MSE], q0[MSE], pv[MSE];
+#pragma unroll
+  for (int m = 0; m < MSE; ++m) {
+    const int i = kb + lane + 32 * m;
+    const bool v = i < R;
+    q0[m] = i;
+    pos[m] = v ? i : (1 << 20);
+    pv[m] = v ? sPerm[i] : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pn[m][k] = v ? St[(i - kb) * 8 + (k ^ swz(i & 7))] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int kr = kb + j;
+    unsigned key = 0u;
+    double2 rcm[MSE];
+#pragma unroll
+    for (int m = 0; m < MSE; ++m) {
+      const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - (pos[m] & 127));
+      // candidates: every remaining row (partial pivoting) or only the row at position kr (PODP_FLAG_NO_PIVOT)
+      if ((PIVOT ? pos[m] >= kr : pos[m] == kr) && pos[m] < R && kk > key) key = kk;
+      rcm[m] = crecip_fast(pn[m][j]);  // speculative: off the chain after the argmax
+    }
+    const unsigned best = __reduce_max_sync(0xffffffffu, key);
+    if ((best >> 7) == 0u) return kr + 1;
+    const int p = 127 - (int)(best & 127u);
+#pragma unroll
+    for (int m = 0; m < MSE; ++m) {
+      if (pos[m] == p) {
+        const double d = fma(pn[m][j].x, pn[m][j].x, pn[m][j].y * pn[m][j].y);
+        sRow[8] = (d >= 1e-290 && d <= 1e290) ? rcm[m] : crecip_slow(pn[m][j]);
+#pragma unroll
+        for (int k = j + 1; k < 8; ++k) sRow[k] = pn[m][k];
+      }
+    }
+    __syncwarp();
+    const double2 rc = sRow[8];
+    double2 u[8];
+#pragma unroll
+    for (int k = j + 1; k < 8; ++k) u[k] = sRow[k];
+#pragma unroll
+    for (int m = 0; m < MSE; ++m) pos[m] = pos[m] == p ? kr : (pos[m] == kr ? p : pos[m]);
+#pragma unroll
+    for (int m = 0; m < MSE; ++m) {
+      const bool act = pos[m] > kr && pos[m] < R;
+      const double2 l = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
+      if (act) pn[m][j] = l;
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k) pn[m][k] = cfms(l, u[k], pn[m][k]);
+    }
+    __syncwarp();  // sRow is rewritten by the next column
+  }
+  // diagonal block L_cc \ U_cc -> strip c rows 0..7
+#pragma unroll
+  for (int m = 0; m < MSE; ++m)
+    if (pos[m] >= kb && pos[m] < kb + 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = pn[m][k];
+    }
+  __syncwarp();
+  // rows below: m L_cc = l  (k = 7 .. 0: m_k = l_k - sum_{jj > k} m_jj L_cc[jj][k]), then store M rows
+  if (kb + 8 < R) {
+#pragma unroll
+    for (int k = 6; k >= 0; --k) {
+#pragma unroll
+      for (int jj = k + 1; jj < 8; ++jj) {
+        const double2 L = St[jj * 8 + (k ^ swz(jj))];
+#pragma unroll
+        for (int m = 0; m < MSE; ++m) pn[m][k] = cfms(pn[m][jj], L, pn[m][k]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MSE; ++m)
+      if (pos[m] >= kb + 8 && pos[m] < R) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = pn[m][k];
+      }
+  }
+  // interchanges: perm and the rows [kb, R) of the strips of earlier panels follow the panel's row movement
+  bool moved = false;
+#pragma unroll
+  for (int m = 0; m < MSE; ++m) moved |= (pos[m] < R && pos[m] != q0[m]);
+  if (__any_sync(0xffffffffu, moved)) {
+#pragma unroll
+    for (int m = 0; m < MSE; ++m)
+      if (pos[m] < R && pos[m] != q0[m]) sPerm[pos[m]] = pv[m];
+    for (int b = 0; b < c; ++b) {
+      double2 *Sb = S + strip_off(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
+#pragma unroll
+      for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
+        double2 tmp[MSE][4];
+#pragma unroll
+        for (int m = 0; m < MSE; ++m)
+          if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tmp[m][k] = Sb[q0[m] * 8 + ((h + k) ^ swz(q0[m] & 7))];
+          }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < MSE; ++m)
+          if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) Sb[pos[m] * 8 + ((h + k) ^ swz(pos[m] & 7))] = tmp[m][k];
+          }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+}  // namespace lull
+
+template <int R, bool PIVOT>
+__global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
+  using C = lull::Cfg<R>;
+  constexpr int NT = C::NT, G = C::G;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r4 = lane >> 2, q = lane & 3;
+  double2 *S = reinterpret_cast<double2 *>(smem_raw + (size_t)wid * C::W_BYTES);
+  double2 *sRow = S + C::STRIP_TILES * 64;
+  int *sPerm = reinterpret_cast<int *>(sRow + 9);
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  const int64_t gw = (int64_t)blockIdx.x * G + wid, nw = (int64_t)gridDim.x * G;
+  double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
+  double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+
+  for (int64_t t = gw; t < total; t += nw) {
+    const int obj = (int)(t / a.F);
+    const int64_t f = t - (int64_t)obj * a.F;
+    const double *op = a.ops + (size_t)obj * a.L.stride;
+    const double om = a.omega[f];
+    const double s = om * op[a.L.scal + SC_NU];
+    const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
+    const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
+    double *Pw = reinterpret_cast<double *>(a.Pws + (size_t)t * 3 * R);
+    int info = isfinite(om) ? 0 : -1;
+    if (info == 0) {
+      for (int i = lane; i < R; i += 32) sPerm[i] = i;
+      __syncwarp();
+      double ar[NT][2], ai[NT][2];
+      for (int c = 0; c < NT; ++c) {
+        // ---- a2: column tile c of A = K + i s M, rows gathered through perm (C fragments) --------------------
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt) {
+          const int ph = sPerm[8 * tt + r4];
+          const double2 *kp = gK + (size_t)ph * R + 8 * c + 2 * q, *mp = gM + (size_t)ph * R + 8 * c + 2 * q;
+          const double2 k0 = __ldg(kp), k1 = __ldg(kp + 1), m0 = __ldg(mp), m1 = __ldg(mp + 1);
+          ar[tt][0] = fma(-s, m0.y, k0.x);
+          ai[tt][0] = fma(s, m0.x, k0.y);
+          ar[tt][1] = fma(-s, m1.y, k1.x);
+          ai[tt][1] = fma(s, m1.x, k1.y);
+        }
+        // ---- a3: left-looking block updates from panels 0..c-1 (DMMA, accumulators stay in registers) ---------
+        for (int b = 0; b < c; ++b) lull::body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
+        // ---- panel c: tiles c..NT-1 -> strip c, then unblocked LU with pivoting --------------------------------
+        {
+          double2 *St = S + lull::strip_off(NT, c) * 64;
+#pragma unroll
+          for (int tt = 0; tt < NT; ++tt) {
+            if (tt >= c) {
+              double2 *row = St + (8 * (tt - c) + r4) * 8;
+              row[(2 * q) ^ lull::swz(r4)] = make_double2(ar[tt][0], ai[tt][0]);
+              row[(2 * q + 1) ^ lull::swz(r4)] = make_double2(ar[tt][1], ai[tt][1]);
+            }
+          }
+        }
+        __syncwarp();
+        if constexpr (C::MS > 1) {
+          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT>(c, S, sRow, sPerm, lane)
+                                  : lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, lane);
+        } else {
+          info = lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, lane);
+        }
+        if (info != 0) break;
+      }
+      if (info == 0) {
+        // ---- right-hand side z = P_perm B (real-ified: cols [Re b_0..2 | Im b_0..2 | 0 0]) and forward sweep ----
+        double z[NT][2];
+        {
+          const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
+          const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
+#pragma unroll
+          for (int tt = 0; tt < NT; ++tt) {
+            const int ph = sPerm[8 * tt + r4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int n = 2 * q + e;
+              double v = 0.0;
+              if (n < 6) {
+                const int d = n < 3 ? n : n - 3;
+                const double2 x0 = __ldg(gb0 + d * R + ph), x1 = __ldg(gb1 + d * R + ph);
+                v = n < 3 ? fma(om, x1.x, x0.x) : fma(om, x1.y, x0.y);
+              }
+              z[tt][e] = v;
+            }
+          }
+        }
+        [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
+          (lull::body_rhs<NT, Bs>(z, S, lane), ...);
+        }(std::make_integer_sequence<int, NT - 1>{});
+        // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----
+        {
+          const int j = lane & 7;
+#pragma unroll 1
+          for (int t0 = 0; t0 < NT; t0 += 4) {
+            const int td = t0 + (lane >> 3);
+            if (td < NT) {
+              const double2 *Dg = S + lull::strip_off(NT, td) * 64;  // rows 0..7 of strip td: L\U diagonal block
+              double2 y[8], x[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                double2 acc = make_double2(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+                for (int k = 0; k < i; ++k) acc = cfms(Dg[i * 8 + (k ^ lull::swz(i))], y[k], acc);
+                y[i] = acc;
+              }
+#pragma unroll
+              for (int i = 7; i >= 0; --i) {
+                double2 acc = y[i];
+#pragma unroll
+                for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ lull::swz(i))], x[k], acc);
+                x[i] = cmul(acc, crecip(Dg[i * 8 + (i ^ lull::swz(i))]));
+              }
+              double2 *dt = gD + td * 64;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+            }
+          }
+        }
+        __syncwarp();
+        // ---- block back substitution x_t = D_t (z_t - sum_{c > t} Y_tc x_c), right-looking over c -------------
+#pragma unroll
+        for (int tt = NT - 1; tt >= 0; --tt) {
+          double b1[2], b2[2];
+          lull::rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
+          const double2 d0 = lull::afrag_cstore(gD + tt * 64, 0, lane), d1 = lull::afrag_cstore(gD + tt * 64, 1, lane);
+          double x0 = 0.0, x1 = 0.0;
+          lull::dmma(x0, x1, d0.x, b1[0]);
+          lull::dmma(x0, x1, d0.y, b2[0]);
+          lull::dmma(x0, x1, d1.x, b1[1]);
+          lull::dmma(x0, x1, d1.y, b2[1]);
+          // P (3 x R complex, direction-major): column n of the real-ified tile = Re (n < 3) / Im (3 <= n < 6)
+          {
+            const int i = 8 * tt + r4;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int n = 2 * q + e;
+              if (n < 6) {
+                const int d = n < 3 ? n : n - 3, part = n < 3 ? 0 : 1;
+                const double v = e ? x1 : x0;
+                Pw[(d * R + i) * 2 + part] = v;
+                if (a.P_out && i < a.r) a.P_out[(((size_t)t * 3 + d) * a.r + i) * 2 + part] = v;
+              }
+            }
+          }
+          if (tt > 0) {
+            lull::rhs_frags(x0, x1, lane, b1, b2);
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              b1[s2] = -b1[s2];
+              b2[s2] = -b2[s2];
+            }
+#pragma unroll
+            for (int t2 = 0; t2 < tt; ++t2) {
+              const double2 *gyt = gY + (tt * (tt - 1) / 2 + t2) * 64;
+              const double2 y0 = lull::afrag_cstore(gyt, 0, lane), y1 = lull::afrag_cstore(gyt, 1, lane);
+              lull::dmma(z[t2][0], z[t2][1], y0.x, b1[0]);
+              lull::dmma(z[t2][0], z[t2][1], y0.y, b2[0]);
+              lull::dmma(z[t2][0], z[t2][1], y1.x, b1[1]);
+              lull::dmma(z[t2][0], z[t2][1], y1.y, b2[1]);
+            }
+          }
+        }
+      }
+    }
+    if (info != 0) {
+      for (int e = lane; e < 6 * R; e += 32) Pw[e] = nanv;
+      if (a.P_out)
+        for (int e = lane; e < 6 * a.r; e += 32) a.P_out[(size_t)t * 6 * a.r + e] = nanv;
+    }
+    if (a.info && lane == 0) a.info[t] = info;
+    __syncwarp();
+  }
+}
+
+namespace lull {
+template <int R>
+static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
+  using C = Cfg<R>;
+  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false> : lu_ll_kernel<R, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+  if (e != cudaSuccess) return e;
+  const int64_t total = (int64_t)a.n_obj * a.F;
+  int64_t blocks = (total + C::G - 1) / C::G;
+  if (blocks > sms) blocks = sms;
+  kern<<<(unsigned)blocks, C::G * 32, C::BYTES, s>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace lull
+
+size_t lu_ll_scratch_bytes(int R, int sms) {
+  if (R % 8 || R > 64) return 0;
+  const int NT = R / 8;
+  int G = 0;
+  switch (R) {
+#define PODP_CASE(RR) \
+  case RR: G = lull::Cfg<RR>::G; break;
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+#undef PODP_CASE
+    default: return 0;
+  }
+  return (size_t)sms * G * (NT * (NT + 1) / 2) * 1024;
+}
+
+cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
+  if (!a.gscr) return cudaErrorInvalidValue;
+  switch (a.L.R) {
+    case 8: return lull::launch_t<8>(a, s, sms);
+    case 16: return lull::launch_t<16>(a, s, sms);
+    case 24: return lull::launch_t<24>(a, s, sms);
+    case 32: return lull::launch_t<32>(a, s, sms);
+    case 40: return lull::launch_t<40>(a, s, sms);
+    case 48: return lull::launch_t<48>(a, s, sms);
+    case 56: return lull::launch_t<56>(a, s, sms);
+    case 64: return lull::launch_t<64>(a, s, sms);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace podp

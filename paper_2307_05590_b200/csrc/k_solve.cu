@@ -119,7 +119,7 @@ size_t solve_scratch_bytes(int R, int sms) {
   return per_warp > 200 * 1024 ? per_warp * (size_t)sms * 4 : 0;
 }
 
-cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch) {
+cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, double2 *gscratch) {
   const int R = a.L.R;
   const size_t per_warp = (size_t)R * (R + 4) * sizeof(double2);
   int dev0 = 0, sms0 = 148;
@@ -130,7 +130,6 @@ cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double
     const int64_t total = (int64_t)a.n_obj * a.F;
     int64_t blocks = total < (int64_t)sms0 * 4 ? total : (int64_t)sms0 * 4;
     solve_smem_kernel<1, true><<<(unsigned)blocks, 32, 0, s>>>(a, gscratch);
-    ++*nlaunch;
     return cudaGetLastError();
   }
   int nw = (int)((200 * 1024) / per_warp);
@@ -156,7 +155,6 @@ cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double
   else if (nw >= 2) PODP_LAUNCH_SOLVE(2)
   else PODP_LAUNCH_SOLVE(1)
 #undef PODP_LAUNCH_SOLVE
-  ++*nlaunch;
   return cudaGetLastError();
 }
 

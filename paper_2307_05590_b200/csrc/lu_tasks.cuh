@@ -4,10 +4,6 @@
 #pragma once
 #include "podp_common.cuh"
 
-#ifndef PODP_LU_TRACE
-#define PODP_LU_TRACE 0
-#endif
-
 namespace podp {
 namespace ludyn {
 
@@ -33,10 +29,7 @@ __device__ __forceinline__ double2 shfl2(double2 v, int src) {
 // an 8-entry shared scratch row.  Returns the first zero-pivot info (0 if none).
 template <int R, int LDA, int MS>
 __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOrig, int *sDst, double2 *sRow, int kb,
-                                            int lane, long long *ftr = nullptr) {
-#define FTR(k) \
-  if (PODP_LU_TRACE && ftr && lane == 0) ftr[k] = clock64()
-  FTR(0);
+                                            int lane) {
   constexpr int NB = 8;
   const unsigned FULL = 0xffffffffu;
   double2 pn[MS][NB];
@@ -49,7 +42,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     for (int c = 0; c < NB; ++c) pn[m][c] = (i < R) ? A[i * LDA + kb + c] : make_double2(0.0, 0.0);
   }
   int info = 0;
-  FTR(1);
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     const int kr = kb + j;
@@ -60,7 +52,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
       if (pos[m] >= kr && pos[m] < R && kk > key) key = kk;
     }
     const unsigned best = __reduce_max_sync(FULL, key);
-    FTR(2 + 3 * j);
     if ((best >> 7) == 0u) {  // exactly zero column (LAPACK getrf info = k+1); no interchange, no elimination
       if (info == 0) info = kr + 1;
       if (lane == 0) sRinv[kr] = make_double2(0.0, 0.0);
@@ -93,7 +84,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     }
 #pragma unroll
     for (int m = 0; m < MS; ++m) pos[m] = (m == ms && lane == src) ? kr : (pos[m] == kr ? p : pos[m]);
-    FTR(3 + 3 * j);
     const double2 rc = crecip_fast(pv);
     if (lane == 0) sRinv[kr] = rc;
 #pragma unroll
@@ -105,7 +95,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
       for (int c = j + 1; c < NB; ++c) pn[m][c] = cfms(l, u[c], pn[m][c]);
     }
     if constexpr (MS > 1) __syncwarp();  // scratch row reused by the next column
-    FTR(4 + 3 * j);
   }
   // write back (L21 multipliers, L11, U11) at the final positions and record the step's permutation
 #pragma unroll
@@ -119,7 +108,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     }
   }
   __syncwarp();
-  FTR(26);
   // L11^{-1} (unit lower) replaces L11 in its slots, so every U(b, .) forms U12 = L11^{-1} (P A12) on DMMA:
   // lane c < 8 solves L11 y = e_c by forward substitution (zeros above c keep the code uniform)
   if (lane < NB) {
@@ -138,8 +126,6 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     for (int j = 1; j < NB; ++j)
       if (j > c) A[(kb + j) * LDA + kb + c] = x[j];
   }
-  FTR(27);
-#undef FTR
   return info;
 }
 

@@ -7,19 +7,25 @@
 #include <cstring>
 #include <string>
 #include <vector>
-#include <cstdlib>
+#include <mutex>
 
 #include "podp_internal.h"
 
 struct podp_ctx {
-  bool pencil_ok;      // pencil precompute available (K positive definite for every object)
-  bool pencil_diag;    // every object has K_R = K and M_I = M: Z^H K_R Z = I, Z^H M_I Z = Lambda exactly
   int device;
   int r;
   int n_obj;
+  int sms;
   podp::Layout L;
   double *d_ops;
-  cudaMemPool_t pool;  // stream-ordered scratch (P hand-off workspace, staging); keeps memory mapped between calls
+  cudaMemPool_t pool;  // stream-ordered scratch (P hand-off workspace, LU scratch); keeps memory mapped between calls
+  // N3 pencil precompute, done lazily by the first PODP_FLAG_PENCIL evaluation (podp_create stays O(r^2) per object)
+  std::vector<double> hK, hM, hb0, hb1;  // per object: r x r, r x r, r x 3, r x 3 complex (host copies)
+  std::vector<char> has_KR_MI;           // per object: K_R or M_I given (pencil coordinates not diagonal)
+  std::mutex pencil_mu;
+  bool pencil_done = false;
+  bool pencil_ok = false;    // K positive definite for every object
+  bool pencil_diag = false;  // every object has K_R = K and M_I = M: Z^H K_R Z = I, Z^H M_I Z = Lambda exactly
 };
 
 namespace {
@@ -215,30 +221,6 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   double *sc = dst + L.scal;
   sc[podp::SC_NU] = o.nu;
   sc[podp::SC_PENCIL_OK] = 0.0;
-  {
-    // pencil precompute on the true r; the padding (K_pad = diag(K, I), M_pad = 0) extends it exactly with
-    // Z_pad = diag(Z, I), lambda_pad = 0, c_pad = 0
-    std::vector<double> Z, lam, c0, c1;
-    if (podp::pencil_precompute(r, o.K, o.M, o.b0, o.b1, Z, lam, c0, c1)) {
-      for (int i = 0; i < R; ++i)
-        for (int j = 0; j < R; ++j) {
-          const size_t e = 2 * ((size_t)i * R + j);
-          const bool in = i < r && j < r;
-          dst[L.Z + e] = in ? Z[2 * ((size_t)i * r + j)] : (i == j ? 1.0 : 0.0);
-          dst[L.Z + e + 1] = in ? Z[2 * ((size_t)i * r + j) + 1] : 0.0;
-        }
-      for (int e = 0; e < r; ++e) dst[L.lam + e] = lam[e];
-      for (int c3 = 0; c3 < 3; ++c3)
-        for (int k = 0; k < r; ++k)
-          for (int c = 0; c < 2; ++c) {
-            dst[L.c0 + 2 * ((size_t)c3 * R + k) + c] = c0[2 * ((size_t)c3 * r + k) + c];
-            dst[L.c1 + 2 * ((size_t)c3 * R + k) + c] = c1[2 * ((size_t)c3 * r + k) + c];
-          }
-      sc[podp::SC_PENCIL_OK] = 1.0;
-      pencil_transform(L, dst);
-      sc[podp::SC_PENCIL_DIAG] = (o.K_R == nullptr && o.M_I == nullptr) ? 1.0 : 0.0;
-    }
-  }
   sc[podp::SC_ALPHA] = o.alpha;
   sc[podp::SC_ALPHA_LB] = o.alpha_lb;
   for (int e = 0; e < 9; ++e) {
@@ -250,6 +232,60 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
 // Padded size: next multiple of 8 (the specialised kernels exist for R = 8, 16, ..., 128); the padding is exact
 // (K_pad = diag(K, I), every other operator zero-padded).
 int choose_R(int r) { return (r + 7) / 8 * 8; }
+
+// N3 precompute for every object (Cholesky, Jacobi, Z, c0, c1 on the true r; the padding extends it exactly with
+// Z_pad = diag(Z, I), lambda_pad = 0, c_pad = 0), then the operators in pencil coordinates; uploads only the
+// pencil blocks.  Called once, under ctx->pencil_mu, by the first PODP_FLAG_PENCIL evaluation.
+podp_status pencil_prepare(podp_ctx *c, cudaStream_t s) {
+  const podp::Layout &L = c->L;
+  const int r = c->r, R = L.R;
+  std::vector<double> host((size_t)L.stride * c->n_obj, 0.0);
+  cudaError_t e = cudaMemcpyAsync(host.data(), c->d_ops, host.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "pencil precompute: download operators");
+  bool ok = true, diag = true;
+  for (int k = 0; k < c->n_obj; ++k) {
+    double *dst = host.data() + (size_t)L.stride * k;
+    std::vector<double> Z, lam, c0, c1;
+    const size_t rr = (size_t)2 * r * r, r3 = (size_t)6 * r;
+    if (!podp::pencil_precompute(r, c->hK.data() + rr * k, c->hM.data() + rr * k, c->hb0.data() + r3 * k,
+                                 c->hb1.data() + r3 * k, Z, lam, c0, c1)) {
+      ok = false;
+      break;
+    }
+    for (int i = 0; i < R; ++i)
+      for (int j = 0; j < R; ++j) {
+        const size_t el = 2 * ((size_t)i * R + j);
+        const bool in = i < r && j < r;
+        dst[L.Z + el] = in ? Z[2 * ((size_t)i * r + j)] : (i == j ? 1.0 : 0.0);
+        dst[L.Z + el + 1] = in ? Z[2 * ((size_t)i * r + j) + 1] : 0.0;
+      }
+    for (int el = 0; el < r; ++el) dst[L.lam + el] = lam[el];
+    for (int c3 = 0; c3 < 3; ++c3)
+      for (int kk = 0; kk < r; ++kk)
+        for (int cc = 0; cc < 2; ++cc) {
+          dst[L.c0 + 2 * ((size_t)c3 * R + kk) + cc] = c0[2 * ((size_t)c3 * r + kk) + cc];
+          dst[L.c1 + 2 * ((size_t)c3 * R + kk) + cc] = c1[2 * ((size_t)c3 * r + kk) + cc];
+        }
+    pencil_transform(L, dst);
+    diag &= !c->has_KR_MI[k];
+  }
+  c->pencil_done = true;
+  c->pencil_ok = ok;
+  c->pencil_diag = ok && diag;
+  if (!ok) return PODP_OK;
+  // the pencil blocks are contiguous from L.Z to the end of each object's stride
+  for (int k = 0; k < c->n_obj && e == cudaSuccess; ++k) {
+    const size_t off = (size_t)L.stride * k + L.Z;
+    e = cudaMemcpyAsync(c->d_ops + off, host.data() + off, sizeof(double) * (L.stride - L.Z), cudaMemcpyHostToDevice, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    c->pencil_ok = false;
+    return cuda_fail(e, "pencil precompute: upload");
+  }
+  return PODP_OK;
+}
 
 }  // namespace
 
@@ -354,10 +390,24 @@ podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int devi
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   podp_ctx *c = new podp_ctx;
-  c->pencil_ok = true;
-  for (int k = 0; k < n_obj; ++k) c->pencil_ok &= host[(size_t)L.stride * k + L.scal + podp::SC_PENCIL_OK] == 1.0;
-  c->pencil_diag = c->pencil_ok;
-  for (int k = 0; k < n_obj; ++k) c->pencil_diag &= host[(size_t)L.stride * k + L.scal + podp::SC_PENCIL_DIAG] == 1.0;
+  {
+    const size_t rr = (size_t)2 * r * r, r3 = (size_t)6 * r;
+    c->hK.resize(rr * n_obj);
+    c->hM.resize(rr * n_obj);
+    c->hb0.resize(r3 * n_obj);
+    c->hb1.resize(r3 * n_obj);
+    c->has_KR_MI.resize(n_obj);
+    for (int k = 0; k < n_obj; ++k) {
+      std::memcpy(c->hK.data() + rr * k, ops[k].K, rr * sizeof(double));
+      std::memcpy(c->hM.data() + rr * k, ops[k].M, rr * sizeof(double));
+      std::memcpy(c->hb0.data() + r3 * k, ops[k].b0, r3 * sizeof(double));
+      std::memcpy(c->hb1.data() + r3 * k, ops[k].b1, r3 * sizeof(double));
+      c->has_KR_MI[k] = ops[k].K_R != nullptr || ops[k].M_I != nullptr;
+    }
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c->sms = sms;
   c->pool = pool;
   c->device = device;
   c->r = r;
@@ -451,21 +501,50 @@ podp_status podp_destroy(podp_ctx *c) {
   return PODP_OK;
 }
 
-podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, double *T1_d, double *I_d,
+podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, double *T1_d, double *I_d,
                       double *Delta_d, int32_t *info_d, double *P_d, int flags, void *cuda_stream) {
   g_err.clear();
   g_last_launches = 0;
+  podp_ctx *c = const_cast<podp_ctx *>(cc);  // only the lazily built pencil precompute is ever written
   if (!c) return fail(PODP_ERR_ARG, "ctx is NULL");
   if (F < 0) return fail(PODP_ERR_ARG, "F < 0");
   if (F == 0) return PODP_OK;
   if (!omega_d || !T1_d || !I_d || !Delta_d) return fail(PODP_ERR_ARG, "null omega/output pointer");
   if ((flags & PODP_FLAG_OUT_P) && !P_d) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P set but P_d is NULL");
-  if ((flags & PODP_FLAG_PENCIL) && !c->pencil_ok)
-    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_PENCIL needs K Hermitian positive definite (Cholesky failed)");
-  if (flags & ~(PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_FLAG_PENCIL | PODP_INTERNAL_FORCE_GENERIC)) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags);
+  const int known = PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_FLAG_PENCIL | PODP_FLAG_LU_LL |
+                    PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC;
+  if (flags & ~known) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
+  const int lu_sel = flags & (PODP_FLAG_LU_LL | PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC);
+  if (lu_sel & (lu_sel - 1)) return fail(PODP_ERR_ARG, "at most one PODP_FLAG_LU_* solver may be requested");
+  const int R = c->L.R;
+  if ((lu_sel == PODP_FLAG_LU_LL && R > 64) || ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && R > 96))
+    return fail(PODP_ERR_UNSUPPORTED, "requested LU kernel is not instantiated for padded r = %d", R);
+  if ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && (flags & PODP_FLAG_NO_PIVOT))
+    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_LU_BLK / _DYN always pivot");
   DeviceGuard guard(c->device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (flags & PODP_FLAG_PENCIL) {
+    std::lock_guard<std::mutex> lk(c->pencil_mu);
+    if (!c->pencil_done) {
+      podp_status st = pencil_prepare(c, s);
+      if (st != PODP_OK) return st;
+    }
+    if (!c->pencil_ok)
+      return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_PENCIL needs K Hermitian positive definite (Cholesky failed)");
+  }
+  // solver: the one-warp left-looking kernel for R <= 64, the blocked multi-warp kernels (measured table) up to 96,
+  // the generic kernel beyond (and for NO_PIVOT above 64)
+  enum { K_LL, K_BLK, K_DYN, K_GEN, K_PENCIL } ker;
+  if (flags & PODP_FLAG_PENCIL) ker = K_PENCIL;
+  else if (lu_sel == PODP_FLAG_LU_LL) ker = K_LL;
+  else if (lu_sel == PODP_FLAG_LU_BLK) ker = K_BLK;
+  else if (lu_sel == PODP_FLAG_LU_DYN) ker = K_DYN;
+  else if (lu_sel == PODP_FLAG_LU_GENERIC) ker = K_GEN;
+  else if (R <= 64) ker = K_LL;
+  else if (flags & PODP_FLAG_NO_PIVOT) ker = K_GEN;
+  else if (R <= 96) ker = (R == 72 || R >= 80) ? K_DYN : K_BLK;
+  else ker = K_GEN;
   podp::EvalArgs a;
   a.ops = c->d_ops;
   a.L = c->L;
@@ -480,28 +559,24 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   a.P_out = (flags & PODP_FLAG_OUT_P) ? P_d : nullptr;
   a.flags = flags;
   a.Pws = nullptr;
-  a.trace = nullptr;
-  static long long *trace_buf = nullptr;
-  if (getenv("PODP_LU_TRACE")) {
-    if (!trace_buf) cudaMallocManaged(&trace_buf, 8 * 1024 * sizeof(long long));
-    cudaMemset(trace_buf, 0, 8 * 1024 * sizeof(long long));
-    cudaDeviceSynchronize();
-    a.trace = trace_buf;
-  }
-  const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * c->L.R * sizeof(double2);
+  a.gscr = nullptr;
+  size_t gsz = 0;
+  if (ker == K_LL) gsz = podp::lu_ll_scratch_bytes(R, c->sms);
+  else if (ker == K_DYN) gsz = podp::lu_dyn_scratch_bytes(R, c->sms);
+  else if (ker == K_GEN) gsz = podp::solve_scratch_bytes(R, c->sms);
+  const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * R * sizeof(double2);
   cudaError_t e = cudaMallocFromPoolAsync((void **)&a.Pws, ws, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
-  a.gscr = nullptr;
-  if (!(flags & PODP_FLAG_PENCIL)) {  // per-group L2 scratch of the dynamically scheduled LU (right-hand sides)
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const size_t gsz = (size_t)sms * 16 * 9 * c->L.R * sizeof(double2);
+  if (gsz) {
     e = cudaMallocFromPoolAsync((void **)&a.gscr, gsz, c->pool, s);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(LU scratch)");
+    if (e != cudaSuccess) {
+      cudaFreeAsync(a.Pws, s);
+      return cuda_fail(e, "cudaMallocAsync(LU scratch)");
+    }
   }
   int nl = 0;
   // N3 without the debug P output: solve for y only and run the MPT/certificate kernel in pencil coordinates
-  const bool pencil_y = (flags & PODP_FLAG_PENCIL) && !(flags & PODP_FLAG_OUT_P) && !getenv("PODP_PENCIL_P");
+  const bool pencil_y = (flags & PODP_FLAG_PENCIL) && !(flags & PODP_FLAG_OUT_P);
   podp::EvalArgs am = a;
   if (pencil_y) {
     am.L.KR = c->L.PKR;
@@ -515,90 +590,23 @@ podp_status podp_eval(const podp_ctx *c, const double *omega_d, int64_t F, doubl
   }
   {
     ProfScope ps("solve", s);
-    // default LU kernel per padded R, measured on B200 (tools/lu_ab.py, F = 1e5): the dynamically scheduled kernel
-    // at R = 40, 56 and >= 72 (3-20 % faster there), the lock-step blocked kernel elsewhere (R <= 32, 48, 64: within
-    // 1-7 %); dev switch PODP_LU_IMPL = b | d | r forces one
-    const char *lv = getenv("PODP_LU_IMPL");
-    const int R = c->L.R;
-    const bool use_blk = lv ? lv[0] == 'b' : !(R == 40 || R == 56 || R >= 72);
-    if ((flags & PODP_FLAG_PENCIL) && pencil_y) e = podp::launch_pencil_y(a, s);
-    else if (flags & PODP_FLAG_PENCIL) e = podp::launch_pencil(a, s);
-    else if (flags & PODP_INTERNAL_FORCE_GENERIC) e = cudaErrorNotSupported;
-    else if ((lv && lv[0] == 'r') || (flags & PODP_FLAG_NO_PIVOT)) e = podp::launch_lu_reg(a, s);
-    else if (use_blk) e = podp::launch_lu_blk(a, s);
-    else e = podp::launch_lu_dyn(a, s);
-    if (e == cudaSuccess) {
-      ++nl;
-    } else if (e == cudaErrorNotSupported) {
-      cudaGetLastError();
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      const size_t gs = podp::solve_scratch_bytes(c->L.R, sms);
-      double2 *gscr = nullptr;
-      if (gs) e = cudaMallocFromPoolAsync((void **)&gscr, gs, c->pool, s);
-      else e = cudaSuccess;
-      if (e == cudaSuccess) e = podp::launch_solve(a, s, &nl, gscr);
-      if (gscr) cudaFreeAsync(gscr, s);
+    switch (ker) {
+      case K_PENCIL: e = pencil_y ? podp::launch_pencil_y(a, s) : podp::launch_pencil(a, s); break;
+      case K_LL: e = podp::launch_lu_ll(a, s, c->sms); break;
+      case K_BLK: e = podp::launch_lu_blk(a, s); break;
+      case K_DYN: e = podp::launch_lu_dyn(a, s); break;
+      case K_GEN: e = podp::launch_solve(a, s, a.gscr); break;
     }
+    if (e == cudaSuccess) ++nl;
   }
   if (e == cudaSuccess) {
     ProfScope ps("mpt", s);
-    e = (flags & PODP_INTERNAL_FORCE_GENERIC) ? cudaErrorNotSupported
-                                              : podp::launch_mpt_tile(am, s, pencil_y && c->pencil_diag);
-    if (e == cudaSuccess) {
-      ++nl;
-    } else if (e == cudaErrorNotSupported) {
-      cudaGetLastError();
-      e = podp::launch_mpt(am, s, &nl);
-    }
+    e = podp::launch_mpt_tile(am, s, pencil_y && c->pencil_diag);
+    if (e == cudaSuccess) ++nl;
   }
   cudaFreeAsync(a.Pws, s);
   if (a.gscr) cudaFreeAsync(a.gscr, s);
   g_last_launches = nl;
-  if (a.trace && getenv("PODP_LU_IMPL") && getenv("PODP_LU_IMPL")[0] == 'd') {  // lu_dyn task records (dev)
-    cudaDeviceSynchronize();
-    const char *kinds[] = {"assemble", "F", "U", "bar", "backsub"};
-    for (int it = 0; it < 2; ++it) {
-      long long t0 = 0;
-      for (int w = 0; w < 8; ++w) {
-        const long long *tr = trace_buf + it * 2048 + w * 256;
-        if (tr[1] && (!t0 || tr[1] < t0)) t0 = tr[1];
-      }
-      for (int w = 0; w < 8; ++w) {
-        const long long *tr = trace_buf + it * 2048 + w * 256;
-        if (!tr[1]) continue;
-        fprintf(stderr, "omega %d warp %d:", it + 1, w);
-        for (int k = 0; k < 80 && tr[3 * k + 1]; ++k) {
-          const long long c = tr[3 * k];
-          fprintf(stderr, " %s(%lld,%lld)[%lld-%lld]", kinds[(c >> 16) & 7], (c >> 8) & 255, c & 255, tr[3 * k + 1] - t0, tr[3 * k + 2] - t0);
-        }
-        fprintf(stderr, "\n");
-      }
-      for (int k = 0; k < 16; ++k) {  // F internals: load | per column: redux, bcast, end | write-back | L11inv
-        const long long *ft = trace_buf + 4096 + it * 1024 + k * 32;
-        if (!ft[0]) continue;
-        fprintf(stderr, "  F%d: load %lld |", k, ft[1] - ft[0]);
-        for (int j = 0; j < 8; ++j)
-          fprintf(stderr, " c%d %lld/%lld/%lld", j, ft[2 + 3 * j] - ft[0], ft[3 + 3 * j] - ft[0], ft[4 + 3 * j] - ft[0]);
-        fprintf(stderr, " | wb %lld | inv %lld\n", ft[26] - ft[0], ft[27] - ft[0]);
-      }
-    }
-  } else if (a.trace) {  // dev instrumentation dump (build with PODP_NVCC_EXTRA=-DPODP_LU_TRACE=1)
-    cudaDeviceSynchronize();
-    for (int q = 1; q < 3; ++q) {
-      const long long *tr = trace_buf + q * 1024;
-      if (!tr[0]) continue;
-      fprintf(stderr, "omega %d: assembled %lld, LU done %lld, back-sub done %lld\n", q, tr[1] - tr[0], tr[2] - tr[0], tr[3] - tr[0]);
-      for (int k = 0; k < 16 && tr[16 + 4 * k]; ++k)
-        fprintf(stderr, "  panel %d: passed hand-off %lld  after lookahead %lld  after own tiles %lld\n", k, tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0]);
-      for (int k = 0; k < 12; ++k) {
-        if (!tr[100 + 8 * k]) continue;
-        fprintf(stderr, "  factor %d cols:", k);
-        for (int j = 0; j < 8; ++j) fprintf(stderr, " %lld", tr[100 + 8 * k + j] - tr[0]);
-        fprintf(stderr, " | loop end %lld | moves done %lld\n", tr[200 + k] - tr[0], tr[210 + k] - tr[0]);
-      }
-    }
-  }
   if (e != cudaSuccess) return cuda_fail(e, "podp_eval launch");
   return PODP_OK;
 }

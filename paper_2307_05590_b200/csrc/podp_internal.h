@@ -39,19 +39,17 @@ struct EvalArgs {
   int32_t *info;
   double *P_out;       // debug P (nullable)
   double2 *Pws;        // workspace: n_obj x F x 3 x R complex (solve -> contraction hand-off)
-  double2 *gscr;       // LU scratch: 16 x SMs groups x 9 R complex (right-hand-side tile + 1/U_kk per group), nullable
+  double2 *gscr;       // LU scratch (kernel-specific size, see the *_scratch_bytes functions), nullable
   int flags;
-  long long *trace;    // dev instrumentation (nullable): clock64 stamps of block 0 / group 0
 };
 
-// Kernel launchers (return cudaGetLastError() after launch; count launches in *nlaunch).
-// Undocumented flag bit (testing only): force the generic shared-memory kernels.
-#define PODP_INTERNAL_FORCE_GENERIC (1 << 16)
-
-cudaError_t launch_lu_reg(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
-cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag = false);  // NotSupported if no instantiation
-cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
-cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s);    // cudaErrorNotSupported if no instantiation
+// Kernel launchers (return cudaGetLastError() after the launch; cudaErrorNotSupported if no instantiation).
+cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms);  // R <= 64, one warp per frequency
+size_t lu_ll_scratch_bytes(int R, int sms);                           // its per-warp L2 scratch (Y_tc, D_t)
+cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);
+cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s);
+size_t lu_dyn_scratch_bytes(int R, int sms);                          // right-hand-side scratch of its RG mode
+cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag = false);
 cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
 cudaError_t launch_pencil_y(const EvalArgs &a, cudaStream_t s);  // N3: y = (I + i s Lambda)^{-1}(c0 + omega c1) only
 cudaError_t launch_invariants(const double *T1, const double *I, int64_t n, double *eigR, double *eigI, cudaStream_t s);
@@ -60,10 +58,8 @@ cudaError_t launch_coil_voltage(const double *T1, const double *I, int64_t n, co
 bool pencil_precompute(int r, const double *K, const double *M, const double *b0, const double *b1,
                        std::vector<double> &Z, std::vector<double> &lam, std::vector<double> &c0,
                        std::vector<double> &c1);
-cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, int *nlaunch, double2 *gscratch);
-// bytes of global scratch launch_solve needs for this R (0 if the shared-memory variant fits)
-size_t solve_scratch_bytes(int R, int sms);
-cudaError_t launch_mpt(const EvalArgs &a, cudaStream_t s, int *nlaunch);
+cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, double2 *gscratch);  // generic: any R, pivot or not
+size_t solve_scratch_bytes(int R, int sms);  // global scratch launch_solve needs for this R (0 if shared fits)
 cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, const double *snap_d, int n_snap,
                           int n_star, double theta, unsigned long long *lam_bits, unsigned long long *arg_idx,
                           double *result_d, cudaStream_t s, int *nlaunch);

@@ -79,11 +79,11 @@ def test_ragged_and_max_r(torch_cuda, r):
 
 @pytest.mark.parametrize("r", [8, 24, 48, 96])
 def test_generic_kernels_parity(torch_cuda, r):
-    """The generic (fallback) kernels stay parity-green: forced with the internal test flag bit 16."""
-    from paper_2307_05590_b200 import FLAG_OUT_R
+    """The generic one-warp LU (PODP_FLAG_LU_GENERIC, the only kernel above padded r = 96) stays parity-green."""
+    from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_LU_GENERIC
     ops = g.make_config0()[0] if r == 8 else g.make_operators(r)
     omega = g.omega_grid(45)
-    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | (1 << 16))
+    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_LU_GENERIC)
     assert (res["info"] == 0).all()
     check_parity(ops, omega, res)
 
@@ -99,12 +99,41 @@ def test_default_flag_outputs_Rt(torch_cuda):
     assert np.array_equal(a["I"], b["I"]) and np.array_equal(a["Delta"], b["Delta"])
 
 
-def test_no_pivot_flag_parity(torch_cuda):
+@pytest.mark.parametrize("r", [8, 48, 64, 96])
+def test_no_pivot_flag_parity(torch_cuda, r):
     from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_NO_PIVOT
-    ops = g.make_operators(48)
+    ops = g.make_operators(r)
     omega = g.omega_grid(97)
     res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_NO_PIVOT)
     check_parity(ops, omega, res)
+
+
+def _lu_flags(r):
+    from paper_2307_05590_b200 import FLAG_LU_LL, FLAG_LU_BLK, FLAG_LU_DYN, FLAG_LU_GENERIC
+    out = [("blk", FLAG_LU_BLK), ("dyn", FLAG_LU_DYN), ("generic", FLAG_LU_GENERIC)]
+    if r <= 64:
+        out.insert(0, ("ll", FLAG_LU_LL))
+    return out
+
+
+@pytest.mark.parametrize("r", [8, 16, 48, 64, 96])
+def test_pivot_forcing_inputs_all_kernels(torch_cuda, r):
+    """K = [[0, B], [B^H, 0]], M = diag(0, CC^H): A(omega) has an exactly zero leading r/2 x r/2 block, so every
+    frequency needs row interchanges.  Every LU kernel must match the oracle (LAPACK zgesv)
+    per entry, and the no-pivot variant must report the zero pivot (info = 1) -- so the suite tells a pivoted LU
+    from an unpivoted one."""
+    from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_NO_PIVOT
+    ops = g.make_pivot_forcing(r, seed=r)
+    omega = g.omega_grid(67)
+    for name, fl in _lu_flags(r):
+        res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | fl, want_P=True)
+        assert (res["info"] == 0).all(), name
+        check_parity(ops, omega, res)
+        for f in range(0, 67, 11):
+            Po = solve_reduced(ops.K, ops.M, ops.b0, ops.b1, ops.nu, float(omega[f]))
+            assert np.linalg.norm(res["P"][0, f].T - Po) / np.linalg.norm(Po) <= 1e-10, name
+    res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_NO_PIVOT)
+    assert (res["info"] == 1).all() and np.isnan(res["T1"]).all()
 
 
 def test_batch_objects_parity(torch_cuda):
@@ -159,26 +188,41 @@ def test_edge_cases_fast_path(torch_cuda, r):
     assert list(res["info"][0]) == [6, 6]
 
 
-@pytest.mark.parametrize("impl", ["b", "d", "d-shared-rhs"])
-@pytest.mark.parametrize("r", [8, 24, 40, 48, 56, 72, 80, 96])
-def test_both_lu_kernels_parity_and_singular(torch_cuda, monkeypatch, impl, r):
-    """Both LU kernels (lock-step blocked 'b', dynamically scheduled 'd'; the default picks one per padded R) stay
-    parity-green on every size class, including a zero pivot at a later panel (LAPACK info = k+1).  At r = 48, 56 and
-    80 the dynamic kernel keeps the right-hand sides in L2 (RG mode); 'd-shared-rhs' forces them into shared memory."""
-    monkeypatch.setenv("PODP_LU_IMPL", impl[0])
-    if impl == "d-shared-rhs":
-        monkeypatch.setenv("PODP_LU_RG", "0")
+@pytest.mark.parametrize("r", [8, 24, 40, 48, 56, 64, 72, 80, 96])
+def test_all_lu_kernels_parity_and_singular(torch_cuda, r):
+    """Every LU kernel (left-looking one-warp 'll' for padded r <= 64, lock-step blocked 'blk', dynamically scheduled
+    'dyn', generic) stays parity-green on every size class, including a non-finite omega and a zero pivot at a
+    later panel (LAPACK info = k+1)."""
+    from paper_2307_05590_b200 import FLAG_OUT_R
     ops = g.make_operators(r, seed=r + 1)
     omega = np.r_[g.omega_grid(61), [np.inf]]
-    res = run_gpu(torch_cuda, ops, omega)
-    assert (res["info"][0][:61] == 0).all() and res["info"][0][61] == -1
-    check_parity(ops, omega, res, sample=range(61))
     d = np.arange(1.0, r + 1)
     k0 = min(r - 1, 13)
     d[k0] = 0.0
     z = g.Operators(**{**ops.__dict__, "K": np.diag(d).astype(complex), "M": np.zeros((r, r), complex)})
-    res = run_gpu(torch_cuda, z, np.array([1.0, 2.0]))
-    assert list(res["info"][0]) == [k0 + 1, k0 + 1] and np.isnan(res["T1"]).all()
+    for name, fl in _lu_flags(r):
+        res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | fl)
+        assert (res["info"][0][:61] == 0).all() and res["info"][0][61] == -1, name
+        check_parity(ops, omega, res, sample=range(61))
+        res = run_gpu(torch_cuda, z, np.array([1.0, 2.0]), flags=FLAG_OUT_R | fl)
+        assert list(res["info"][0]) == [k0 + 1, k0 + 1] and np.isnan(res["T1"]).all(), name
+
+
+def test_lu_kernel_selection_errors(torch_cuda):
+    from paper_2307_05590_b200 import Evaluator, PodpError, FLAG_LU_LL, FLAG_LU_BLK, FLAG_NO_PIVOT
+    torch = torch_cuda
+    ev = Evaluator(g.make_operators(96))
+    w = torch.tensor(g.omega_grid(5), device="cuda")
+    with pytest.raises(PodpError) as ei:
+        ev.eval(w, flags=FLAG_LU_LL)            # not instantiated above padded r = 64
+    assert ei.value.status == 4
+    with pytest.raises(PodpError) as ei:
+        ev.eval(w, flags=FLAG_LU_LL | FLAG_LU_BLK)
+    assert ei.value.status == 1
+    with pytest.raises(PodpError) as ei:
+        ev.eval(w, flags=FLAG_LU_BLK | FLAG_NO_PIVOT)
+    assert ei.value.status == 4
+    ev.close()
 
 
 def test_invariants_scaling_bitwise(torch_cuda):
@@ -350,6 +394,18 @@ def test_pencil_batch_and_unsupported(torch_cuda):
         ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_PENCIL)
     assert ei.value.status == 4
     ev.close()
+
+
+@pytest.mark.parametrize("r", [8, 48, 96])
+def test_pencil_illconditioned_K(torch_cuda, r):
+    """N3 on a K with condition number 1e8 (its Z = L^{-H} V has condition number 1e4): still per-entry parity."""
+    from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_PENCIL
+    ops = g.make_illconditioned(r, 1e8, seed=r)
+    omega = g.omega_grid(53)
+    for fl in (FLAG_OUT_R | FLAG_PENCIL, FLAG_OUT_R):
+        res = run_gpu(torch_cuda, ops, omega, flags=fl)
+        assert (res["info"] == 0).all()
+        check_parity(ops, omega, res)
 
 
 def test_N4_invariants_and_voltage_parity(torch_cuda):
