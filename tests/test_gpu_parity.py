@@ -398,14 +398,40 @@ def test_pencil_batch_and_unsupported(torch_cuda):
 
 @pytest.mark.parametrize("r", [8, 48, 96])
 def test_pencil_illconditioned_K(torch_cuda, r):
-    """N3 on a K with condition number 1e8 (its Z = L^{-H} V has condition number 1e4): still per-entry parity."""
+    """N3 on ill-conditioned K (its Z = L^{-H} V has condition number sqrt(kappa(K))).
+
+    kappa = 1e4: the standard gate against the FP64 oracle.  kappa = 1e8: there the FP64 oracle itself is only
+    accurate to ~kappa u (1-2e-9 against an 80-bit LU, measured), and two FP64 methods that do not share rounding
+    (LAPACK LU vs Cholesky + eigen pencil) differ by that much; SURVEY 8(c)'s adjudication rule applies: each GPU
+    path's error against the 80-bit re-evaluation (oracle/extended.py) must be <= 4x the FP64 oracle's own error
+    there (or <= 1e-10).  The LU kernel additionally keeps the 1e-10 gate against the FP64 oracle."""
+    from oracle.extended import evaluate_one_ld
     from paper_2307_05590_b200 import FLAG_OUT_R, FLAG_PENCIL
-    ops = g.make_illconditioned(r, 1e8, seed=r)
+    ops = g.make_illconditioned(r, 1e4, seed=r)
     omega = g.omega_grid(53)
     for fl in (FLAG_OUT_R | FLAG_PENCIL, FLAG_OUT_R):
         res = run_gpu(torch_cuda, ops, omega, flags=fl)
         assert (res["info"] == 0).all()
         check_parity(ops, omega, res)
+    ops = g.make_illconditioned(r, 1e8, seed=r)
+    omega = g.omega_grid(29)
+    res_lu = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R)
+    check_parity(ops, omega, res_lu)
+    res_pe = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | FLAG_PENCIL)
+    assert (res_pe["info"] == 0).all()
+    worst_ratio = 0.0
+    for f, w in enumerate(omega):
+        w = float(w)
+        t = evaluate_one_ld(ops, w)
+        o = oracle.evaluate_one(ops, w, out_R=True)
+        eo = errors(ops, w, oracle.to6(o["R"]), oracle.to6(o["I"]), oracle.to6(o["Delta"]), t["R6"], t["I6"], t["D6"])
+        for res in (res_lu, res_pe):
+            eg = errors(ops, w, res["T1"][0, f], res["I"][0, f], res["Delta"][0, f], t["R6"], t["I6"], t["D6"])
+            for k, tol in ((0, TOL_RI), (1, TOL_RI), (2, TOL_DELTA)):
+                bound = np.maximum(tol, 4.0 * eo[k])
+                assert np.all(eg[k] <= bound), (w, k, eg[k], eo[k])
+                worst_ratio = max(worst_ratio, float(np.max(eg[k] / np.maximum(eo[k], tol))))
+    print(f"r={r} kappa=1e8: worst GPU/oracle error ratio against 80-bit {worst_ratio:.3g}")
 
 
 def test_N4_invariants_and_voltage_parity(torch_cuda):

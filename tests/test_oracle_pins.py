@@ -355,3 +355,89 @@ def test_N4_voltage_pins():
     Rd = np.array([[1.0, 2.0, 3.0, 0, 0, 0]]); Id = np.array([[0.5, 0.0, -1.0, 0, 0, 0]])
     v = oracle.coil_voltage(Rd, Id, [[0, 0, 2.0]], [[0, 0, 3.0]])
     assert v[0, 0] == (3.0 - 1.0j) * 6.0
+
+
+# ---------------------------------------------------------------- parity metric pins
+# The gate's denominators (oracle/parity.py magnitudes(), SURVEY 8(c) "Parity metric") must bound the values they
+# normalise (Cauchy-Schwarz in the K_R / M inner products, triangle inequality), and reduce to the value itself in
+# the cases where no cancellation is possible -- so a slip that inflates them (a lost sqrt, a dropped factor)
+# fails here instead of silently loosening the 1e-10 gate.
+def _sweep_cases():
+    cases = [("c0", g.make_config0()[0], g.omega_grid(9))]
+    for r in (24, 48, 32, 96):
+        cases.append((f"r{r}", g.make_operators(r), g.omega_grid(7)))
+    cases.append(("pivot-forcing", g.make_pivot_forcing(16, seed=3), g.omega_grid(7)))
+    cases.append(("kappa1e8", g.make_illconditioned(8, 1e8, seed=8), g.omega_grid(7)))
+    return cases
+
+
+@pytest.mark.parametrize("name,ops,omegas", _sweep_cases(), ids=lambda x: x if isinstance(x, str) else "")
+def test_parity_magnitudes_bound_values(name, ops, omegas):
+    from oracle.parity import magnitudes
+    for w in omegas:
+        o = oracle.evaluate_one(ops, float(w), out_R=True)
+        magR, magI, magD = magnitudes(ops, float(w), o["P"])
+        R6, I6, D6 = oracle.to6(o["R"]), oracle.to6(o["I"]), oracle.to6(o["Delta"])
+        tol = 1e-12
+        assert np.all(np.abs(R6) <= magR * (1 + tol)), name
+        assert np.all(np.abs(I6) <= magI * (1 + tol)), name
+        assert np.all(D6 <= magD * (1 + tol)), name
+        K_R = ops.K if ops.K_R is None else ops.K_R
+        if np.linalg.eigvalsh(K_R)[0] > 0:
+            # diagonal R entries: no cancellation, |R_ii| = (alpha^3/4) p_i^H K_R p_i = mag^R_ii exactly
+            assert np.allclose(np.abs(R6[:3]), magR[:3], rtol=1e-13, atol=0), name
+
+
+def test_parity_magnitudes_equality_cases(c0, c1ops):
+    """mag^I_ii = |I_ii| when S = 0 and H = 0 (only the nu p^H M p term; config 0's M is full rank, so p^H M p has
+    no cancellation); mag^Delta_ii = 3 Delta_ii when P = 0 and G has non-negative real entries
+    (w_i = e_2i + omega e_2i+1 >= 0, so |w|^T |G| |w| = w^T G w = n_i)."""
+    from oracle.parity import magnitudes
+    o = c0[0]
+    ops = g.Operators(**{**o.__dict__, "S": np.zeros((3, 3)), "H": np.zeros_like(o.H)})
+    for w in (10.0, 1e4, 1e8):
+        ev = oracle.evaluate_one(ops, w, out_R=True)
+        _, magI, _ = magnitudes(ops, w, ev["P"])
+        assert np.allclose(np.abs(oracle.to6(ev["I"])[:3]), magI[:3], rtol=1e-13, atol=0)
+    o = c1ops
+    rng = np.random.default_rng(5)
+    Wr = rng.uniform(0.0, 1.0, (o.G.shape[0], o.G.shape[0]))
+    ops0 = g.Operators(**{**o.__dict__, "b0": np.zeros_like(o.b0), "b1": np.zeros_like(o.b1),
+                          "G": (Wr.T @ Wr).astype(np.complex128)})
+    for w in (10.0, 1e4, 1e8):
+        ev = oracle.evaluate_one(ops0, w, out_R=True)
+        _, _, magD = magnitudes(ops0, w, ev["P"])
+        D6 = oracle.to6(ev["Delta"])
+        assert np.allclose(magD[:3], 3.0 * D6[:3], rtol=1e-13, atol=0)
+
+
+# ---------------------------------------------------------------- 80-bit adjudication oracle (oracle/extended.py)
+def test_extended_oracle_matches_fp64_when_well_conditioned(c1ops):
+    from oracle.extended import evaluate_one_ld
+    from oracle.parity import errors
+    for w in (10.0, 3.7e3, 2.2e6, 1e8):
+        e = evaluate_one_ld(c1ops, w)
+        o = oracle.evaluate_one(c1ops, w, out_R=True)
+        eR, eI, eD = errors(c1ops, w, e["R6"], e["I6"], e["D6"], oracle.to6(o["R"]), oracle.to6(o["I"]),
+                            oracle.to6(o["Delta"]))
+        assert eR.max() <= 1e-11 and eI.max() <= 1e-11 and eD.max() <= 1e-9
+
+
+def test_extended_oracle_solve_residual_and_scalar_closed_form():
+    from oracle.extended import CLD, evaluate_one_ld, solve_ld
+    ops = g.make_illconditioned(8, 1e8, seed=8)
+    s = 1e7 * ops.nu
+    A = ops.K.astype(CLD) + CLD(1j) * CLD(s) * ops.M.astype(CLD)
+    B = ops.b0.astype(CLD) + CLD(1e7) * ops.b1.astype(CLD)
+    X = solve_ld(A, B)
+    res = np.abs(A @ X - B).max() / (np.abs(A).max() * np.abs(X).max())
+    assert res < 1e-17  # long double unit roundoff 5.4e-20, r = 8
+    # r = 1 closed form (pin C2 in long double): p = (b0 + w b1)/(k + i w nu m)
+    k, m, b0, b1, w = 3.0, 0.5, 1 + 2j, -0.25 + 1j, 1e3
+    one = g.Operators(K=np.array([[k + 0j]]), M=np.array([[m + 0j]]), b0=np.full((1, 3), b0),
+                      b1=np.full((1, 3), b1), N0=np.eye(3), S=np.zeros((3, 3)), H=np.zeros((3, 1), complex),
+                      G=np.eye(8, dtype=complex), nu=0.1, alpha=1.0, alpha_lb=1.0)
+    e = evaluate_one_ld(one, w)
+    p = (b0 + w * b1) / (k + 1j * w * 0.1 * m)
+    assert abs(e["P"][0, 0] - p) <= 1e-15 * abs(p)
+    assert abs(e["R6"][0] - (-0.25 * k * abs(p) ** 2)) <= 1e-15 * 0.25 * k * abs(p) ** 2
