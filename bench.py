@@ -108,18 +108,24 @@ class ClockSampler:
 
 def oracle_sample(ops, omega, workers: int):
     """Time the CPU oracle (as it stands) over `omega` on `workers` processes; returns (seconds, n)."""
+    return oracle_tasks([(ops, omega)], workers)
+
+
+def oracle_tasks(tasks, workers: int):
+    """Time the CPU oracle over a list of (ops, omegas) tasks, frequencies dealt round-robin to `workers` spawned
+    processes with single-threaded BLAS; returns (seconds, n_frequencies)."""
     import multiprocessing as mp
     env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
     saved = {k: os.environ.get(k) for k in env_keys}
     for k in env_keys:
         os.environ[k] = "1"
     try:
-        chunks = [omega[i::workers] for i in range(workers)]
+        chunks = [[(o, om[i::workers]) for (o, om) in tasks] for i in range(workers)]
         ctx = mp.get_context("spawn")
         with ctx.Pool(workers) as pool:
-            pool.map(_oracle_chunk, [(ops, omega[:2])] * workers)  # warm the workers (imports)
+            pool.map(_oracle_chunk, [[(tasks[0][0], tasks[0][1][:2])]] * workers)  # warm the workers (imports)
             t0 = time.perf_counter()
-            pool.map(_oracle_chunk, [(ops, c) for c in chunks])
+            pool.map(_oracle_chunk, chunks)
             dt = time.perf_counter() - t0
     finally:
         for k, v in saved.items():
@@ -127,14 +133,17 @@ def oracle_sample(ops, omega, workers: int):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
-    return dt, len(omega)
+    return dt, sum(len(om) for (_o, om) in tasks)
 
 
-def _oracle_chunk(args):
-    ops, om = args
+def _oracle_chunk(tasks):
     import oracle
-    oracle.evaluate(ops, om, out_R=False)
-    return len(om)
+    n = 0
+    for ops, om in tasks:
+        if len(om):
+            oracle.evaluate(ops, om, out_R=False)
+        n += len(om)
+    return n
 
 
 def host_cores() -> int:
@@ -142,6 +151,82 @@ def host_cores() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+def measure_config(k: int, steps: int, warmup: int, dev, flush, cpu_seconds: float, cpu: bool) -> dict:
+    """Secondary BASELINE configs: one step = podp_eval over the config's frequencies (all
+    objects for c3) + podp_select for single-object configs (c4: one Algorithm-1 iteration over 13 log-spaced
+    snapshots, N* = 2).  Device-timed with CUDA events, L2 flushed between steps; kernel split from the library's
+    event instrumentation; cpu_baseline = the oracle on a bounded evenly spaced sample of the same workload."""
+    import numpy as np
+    import torch
+    import podp_inputs as g
+    import paper_2307_05590_b200 as pb
+    c = g.make_config(k)
+    spec = c["spec"]
+    r, F, n_obj = spec["r"], spec["F"], len(c["ops"])
+    ev = pb.Evaluator(c["ops"], device=dev.index)
+    w = torch.tensor(c["omega"], device=dev)
+    out = ev.alloc_outputs(F)
+    snap = c.get("snap", g.snapshot_grid(13))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ev.eval(w, out=out)
+        n = ev.launches_last_call()
+        if n_obj == 1:
+            ev.select(w, out["Delta"][0], snap, n_star=2)
+            n += ev.launches_last_call()
+        return n
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    pb.profile_enable(True)
+    pb.profile_read(reset=True)
+    tot, launches = 0.0, 0
+    for _ in range(steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches += step()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    prof = pb.profile_read(reset=True)
+    pb.profile_enable(False)
+    ev.close()
+    n_eval = F * n_obj
+    value = n_eval * steps / (tot / 1e3)
+    res = {"workload": spec["name"], "r": r, "F": F, "n_obj": n_obj, "evaluations_per_step": n_eval,
+           "step": "podp_eval + podp_select" if n_obj == 1 else "podp_eval (batch of objects)",
+           "value": value, "unit": UNIT, "ms_per_step": tot / steps, "steps": steps,
+           "pct_fp64_peak_falg": 100.0 * falg(r) * value / 1e12 / FP64_PEAK_TFLOPS,
+           "kernel_ms_per_step": {kk: v[0] / steps for kk, v in prof.items()},
+           "gpu_launches": launches}
+    if "solve" in prof:
+        res["solve_frac_fp64_peak"] = falg_solve(r) * n_eval / (prof["solve"][0] / steps / 1e3) / 1e12 / FP64_PEAK_TFLOPS
+    if cpu:
+        cores = host_cores()
+        # bounded sample: evenly spaced frequencies (and objects, c3) sized for ~cpu_seconds of oracle work
+        rate = {8: 20000.0, 24: 4000.0, 32: 2500.0, 48: 1100.0, 96: 320.0}.get(r, 1000.0) * cores
+        n_s = int(max(cores * 4, min(n_eval, rate * cpu_seconds)))
+        if n_obj == 1:
+            idx = np.linspace(0, F - 1, n_s).astype(int)
+            tasks = [(c["ops"][0], c["omega"][idx])]
+            what = f"{n_s} of the {F} frequencies, evenly spaced"
+        else:
+            n_o = min(n_obj, 32)
+            objs = np.linspace(0, n_obj - 1, n_o).astype(int)
+            per = max(1, n_s // n_o)
+            fi = np.linspace(0, F - 1, per).astype(int)
+            tasks = [(c["ops"][j], c["omega"][fi]) for j in objs]
+            what = f"{per} evenly spaced frequencies x {n_o} evenly spaced objects"
+        dt, n = oracle_tasks(tasks, cores)
+        res["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"{what} ({dt:.1f} s, {cores} worker processes x 1 BLAS thread)"}
+    return res
 
 
 def run_reference(args, rank: int, world: int):
@@ -186,6 +271,8 @@ def main():
     ap.add_argument("--F", type=int, default=F_HEAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-adapt", action="store_true", help="skip the Algorithm-1 (N2) variant")
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary BASELINE configs c0, c1, c3, c4")
+    ap.add_argument("--configs", default="0,1,3,4", help="secondary BASELINE configs measured into 'configs'")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -319,6 +406,16 @@ def main():
                 "note": "host clock around synchronised phases; online = podp_create + podp_eval + podp_select"}
         except Exception as exc:  # pragma: no cover
             variants["adaptive_N2"] = {"error": str(exc)[:200]}
+    # secondary BASELINE configs (rank 0, N = 1 only: they are single-GPU workloads)
+    configs = {}
+    if rank == 0 and world == 1 and not args.no_configs:
+        for k in [int(x) for x in args.configs.split(",") if x.strip()]:
+            try:
+                configs[f"c{k}"] = measure_config(k, min(args.steps, 5), 3, dev, flush,
+                                                  float(os.environ.get("PODP_CPU_SECONDS_CFG", "3")),
+                                                  not args.no_cpu_baseline)
+            except Exception as exc:  # pragma: no cover
+                configs[f"c{k}"] = {"error": str(exc)[:200]}
     total_ms = float(sum(step_ms))
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
@@ -390,6 +487,8 @@ def main():
             "gpu_launches": launches,
             "variants": variants,
         }
+        if configs:
+            line["configs"] = configs
         line["clocks"] = clk.summary()
         if not args.no_cpu_baseline:
             cores = host_cores()

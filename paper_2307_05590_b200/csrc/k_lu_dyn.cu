@@ -450,9 +450,9 @@ size_t lu_dyn_scratch_bytes(int R, int sms) { return (size_t)sms * 16 * 9 * R * 
 
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80
-  // (R = 56 and 80 with the right-hand sides in L2: 4 instead of 3, 2 instead of 1 groups per SM), four at R = 64,
-  // 88 and 96
+  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80,
+  // four at R = 64, 88 and 96.  The right-hand-side-in-L2 (RG) variant is instantiated only where it buys a group
+  // per SM (launch_lu_dyn_t): R = 48 (6 instead of 5) and R = 56 (4 instead of 3); at R = 80 both layouts fit 2
   const int R = a.L.R;
   const int wv = (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4));
   switch (R) {

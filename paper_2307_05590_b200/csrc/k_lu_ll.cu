@@ -25,6 +25,12 @@
 
 #include "podp_common.cuh"
 
+// Dev-only phase ablation for throughput attribution (never defined in the product build): bit 0 skips the panel's
+// arithmetic, 1 the left-looking updates, 2 the diagonal-block inverses, 3 the forward/back substitution.
+#ifndef PODP_LL_ABLATE
+#define PODP_LL_ABLATE 0
+#endif
+
 namespace podp {
 
 namespace lull {
@@ -37,7 +43,11 @@ struct Cfg {
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
   static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16;
   static constexpr int G_SMEM = (227 * 1024) / W_BYTES;
+#ifdef PODP_LL_G  // dev: fewer warps per CTA (occupancy experiments)
+  static constexpr int G = G_SMEM < PODP_LL_G ? G_SMEM : PODP_LL_G;
+#else
   static constexpr int G = G_SMEM < 16 ? G_SMEM : 16;    // warps (= concurrent frequencies) per CTA
+#endif
   static constexpr int GSCR_TILES = NT * (NT + 1) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT
   static constexpr size_t BYTES = (size_t)G * W_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
@@ -168,7 +178,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
   constexpr int NT = R / 8;
   const int kb = 8 * c;
   double2 *St = S + strip_off(NT, c) * 64;
-  double2 pn[MSE][8];
+  double2 pn[MSE][8], urc[MSE];
   int pos[MSE], q0[MSE], pv[MSE];
 #pragma unroll
   for (int m = 0; m < MSE; ++m) {
@@ -210,7 +220,10 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
 #pragma unroll
     for (int k = j + 1; k < 8; ++k) u[k] = sRow[k];
 #pragma unroll
-    for (int m = 0; m < MSE; ++m) pos[m] = pos[m] == p ? kr : (pos[m] == kr ? p : pos[m]);
+    for (int m = 0; m < MSE; ++m) {
+      pos[m] = pos[m] == p ? kr : (pos[m] == kr ? p : pos[m]);
+      if (pos[m] == kr) urc[m] = rc;  // 1/U_kk, kept for the diagonal-block inverse
+    }
 #pragma unroll
     for (int m = 0; m < MSE; ++m) {
       const bool act = pos[m] > kr && pos[m] < R;
@@ -221,12 +234,14 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     }
     __syncwarp();  // sRow is rewritten by the next column
   }
-  // diagonal block L_cc \ U_cc -> strip c rows 0..7
+  // diagonal block L_cc \ U_cc -> strip c rows 0..7, with 1/U_kk stored in place of U_kk (the diagonal entries
+  // are used only by the diagonal-block inverse D_c, which needs the reciprocals)
 #pragma unroll
   for (int m = 0; m < MSE; ++m)
     if (pos[m] >= kb && pos[m] < kb + 8) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = pn[m][k];
+      for (int k = 0; k < 8; ++k)
+        St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = (k == pos[m] - kb) ? urc[m] : pn[m][k];
     }
   __syncwarp();
   // rows below: m L_cc = l  (k = 7 .. 0: m_k = l_k - sum_{jj > k} m_jj L_cc[jj][k]), then store M rows
@@ -326,7 +341,8 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
           ai[tt][1] = fma(s, m1.x, k1.y);
         }
         // ---- a3: left-looking block updates from panels 0..c-1 (DMMA, accumulators stay in registers) ---------
-        for (int b = 0; b < c; ++b) lull::body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
+        if constexpr (!(PODP_LL_ABLATE & 2))
+          for (int b = 0; b < c; ++b) lull::body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
         // ---- panel c: tiles c..NT-1 -> strip c, then unblocked LU with pivoting --------------------------------
         {
           double2 *St = S + lull::strip_off(NT, c) * 64;
@@ -340,7 +356,9 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
           }
         }
         __syncwarp();
-        if constexpr (C::MS > 1) {
+        if constexpr (PODP_LL_ABLATE & 1) {
+          info = 0;
+        } else if constexpr (C::MS > 1) {
           info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT>(c, S, sRow, sPerm, lane)
                                   : lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, lane);
         } else {
@@ -370,11 +388,12 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
             }
           }
         }
-        [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
-          (lull::body_rhs<NT, Bs>(z, S, lane), ...);
-        }(std::make_integer_sequence<int, NT - 1>{});
+        if constexpr (!(PODP_LL_ABLATE & 8))
+          [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
+            (lull::body_rhs<NT, Bs>(z, S, lane), ...);
+          }(std::make_integer_sequence<int, NT - 1>{});
         // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----
-        {
+        if constexpr (!(PODP_LL_ABLATE & 4)) {
           const int j = lane & 7;
 #pragma unroll 1
           for (int t0 = 0; t0 < NT; t0 += 4) {
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
                 double2 acc = y[i];
 #pragma unroll
                 for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ lull::swz(i))], x[k], acc);
-                x[i] = cmul(acc, crecip(Dg[i * 8 + (i ^ lull::swz(i))]));
+                x[i] = cmul(acc, Dg[i * 8 + (i ^ lull::swz(i))]);  // 1/U_ii (stored by the panel)
               }
               double2 *dt = gD + td * 64;
 #pragma unroll
@@ -428,7 +447,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
               }
             }
           }
-          if (tt > 0) {
+          if (tt > 0 && !(PODP_LL_ABLATE & 8)) {
             lull::rhs_frags(x0, x1, lane, b1, b2);
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {

@@ -118,6 +118,17 @@ def _per_entry_parity(ops, out):
     return oD
 
 
+def _check_lambda(ops, oD, rec):
+    """Lambda of the final certification: GPU select vs the oracle's select on the oracle's Delta of the same ROM,
+    under the Delta gate at the maximising entry (1e-8 x max(Delta, 1e-6 mag^Delta): near-zero residuals are
+    cancellation-limited)."""
+    from oracle.parity import TOL_DELTA, magnitudes
+    oLam = oracle.select(OMEGA, oD, rec["snap"], 2)[2]
+    f, e = np.argwhere(oD == oLam)[0]
+    magD = magnitudes(ops, float(OMEGA[f]))[2][e]
+    assert abs(rec["Lambda"] - oLam) <= TOL_DELTA * max(oLam, 1e-6 * magD)
+
+
 @pytest.mark.gpu
 def test_N2_gpu_driver_matches_oracle(torch_cuda, fom, vol, run4):
     from paper_2307_05590_b200 import FLAG_OUT_R, adapt
@@ -129,9 +140,7 @@ def test_N2_gpu_driver_matches_oracle(torch_cuda, fom, vol, run4):
         assert a["snap"] == b["snap"] and a["new"] == b["new"]        # every greedy decision identical
         assert abs(a["Lambda"] - b["Lambda"]) <= 1e-2 * b["Lambda"]   # different ROMs (off-line rounding)
     oD_same = _per_entry_parity(ops, out)
-    # Lambda of the final certification: GPU select vs the oracle's select on the oracle's Delta of the same ROM
-    oLam = oracle.select(OMEGA, oD_same, h[-1]["snap"], 2)[2]
-    assert abs(h[-1]["Lambda"] - oLam) <= 1e-8 * oLam
+    _check_lambda(ops, oD_same, h[-1])
 
 
 def test_N2_oracle_per_direction_runs(fom, vol):
@@ -151,5 +160,4 @@ def test_N2_gpu_driver_per_direction_matches_oracle(torch_cuda, fom, vol):
         assert a["m"] == b["m"] and a["snap"] == b["snap"] and a["new"] == b["new"]
         assert abs(a["Lambda"] - b["Lambda"]) <= 1e-2 * b["Lambda"]
     oD_same = _per_entry_parity(ops, out)
-    oLam = oracle.select(OMEGA, oD_same, h[-1]["snap"], 2)[2]
-    assert abs(h[-1]["Lambda"] - oLam) <= 1e-8 * oLam
+    _check_lambda(ops, oD_same, h[-1])
