@@ -223,9 +223,13 @@ def measure_config(k: int, steps: int, warmup: int, dev, flush, cpu_seconds: flo
             fi = np.linspace(0, F - 1, per).astype(int)
             tasks = [(c["ops"][j], c["omega"][fi]) for j in objs]
             what = f"{per} evenly spaced frequencies x {n_o} evenly spaced objects"
-        dt, n = oracle_tasks(tasks, cores)
+        dt, n, passes = 0.0, 0, 0
+        while dt < cpu_seconds and passes < 50:  # whole passes over the sample until >= cpu_seconds of CPU work
+            d, k = oracle_tasks(tasks, cores)
+            dt, n, passes = dt + d, n + k, passes + 1
         res["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-                               "sample": f"{what} ({dt:.1f} s, {cores} worker processes x 1 BLAS thread)"}
+                               "sample": f"{passes} pass(es) over {what} ({dt:.1f} s, {cores} worker processes x "
+                                         f"1 BLAS thread)"}
     return res
 
 
