@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(lublk::Cfg<R, W>::THREADS, 1) lu_blk_kernel(Ev
       for (int c = j + 1; c < NB; ++c) u[c] = sRowP[c];
 #pragma unroll
       for (int m = 0; m < MS; ++m) pos[m] = mine[m] ? kr : (pos[m] == kr ? p : pos[m]);
-      const double2 rc = crecip_fast(pv);
+      // pivots with |p|^2 outside the normal range take the call-free scaled reciprocal (uniform branch)
+      const double pd = fma(pv.x, pv.x, pv.y * pv.y);
+      const double2 rc = (pd >= 1e-290 && pd <= 1e290) ? crecip_fast(pv) : crecip_scaled(pv);
       if (lane == 0) sRinv[kr] = rc;
 #pragma unroll
       for (int m = 0; m < MS; ++m) {

@@ -446,15 +446,39 @@ static cudaError_t launch_lu_dyn_k(const EvalArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-size_t lu_dyn_scratch_bytes(int R, int sms) { return (size_t)sms * 16 * 9 * R * sizeof(double2); }
+// measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80,
+// four at R = 64, 88 and 96.  The right-hand-side-in-L2 (RG) variant is instantiated only where it buys a group
+// per SM (launch_lu_dyn_t): R = 48 (6 instead of 5) and R = 56 (4 instead of 3); at R = 80 both layouts fit 2
+static int dyn_warps(int R) { return R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4); }
+
+template <int R>
+static bool dyn_uses_rg() {
+  switch (dyn_warps(R)) {
+    case 1: return ludyn::Cfg<R, 1, true>::GROUPS > ludyn::Cfg<R, 1, false>::GROUPS;
+    case 2: return ludyn::Cfg<R, 2, true>::GROUPS > ludyn::Cfg<R, 2, false>::GROUPS;
+    default: return ludyn::Cfg<R, 4, true>::GROUPS > ludyn::Cfg<R, 4, false>::GROUPS;
+  }
+}
+
+// L2 scratch of the RG variant; 0 where the launch uses the shared-memory layout (no 16 MB allocation
+// per evaluation for nothing)
+size_t lu_dyn_scratch_bytes(int R, int sms) {
+  bool rg = false;
+  switch (R) {
+#define PODP_CASE(RR) \
+  case RR: rg = dyn_uses_rg<RR>(); break;
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+    PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
+#undef PODP_CASE
+    default: break;
+  }
+  return rg ? (size_t)sms * 16 * 9 * R * sizeof(double2) : 0;
+}
 
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s) {
   if (a.flags & PODP_FLAG_NO_PIVOT) return cudaErrorNotSupported;
-  // measured on B200 (tools/lu_ab.py, F = 1e5): one warp per frequency up to R = 40, two at R = 48, 56, 72 and 80,
-  // four at R = 64, 88 and 96.  The right-hand-side-in-L2 (RG) variant is instantiated only where it buys a group
-  // per SM (launch_lu_dyn_t): R = 48 (6 instead of 5) and R = 56 (4 instead of 3); at R = 80 both layouts fit 2
   const int R = a.L.R;
-  const int wv = (R <= 40 ? 1 : ((R == 48 || R == 56 || R == 72 || R == 80) ? 2 : 4));
+  const int wv = dyn_warps(R);
   switch (R) {
 #define PODP_CASE(RR)                                     \
   case RR:                                                \

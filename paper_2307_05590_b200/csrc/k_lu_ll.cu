@@ -26,7 +26,8 @@
 #include "podp_common.cuh"
 
 // Dev-only phase ablation for throughput attribution (never defined in the product build): bit 0 skips the panel's
-// arithmetic, 1 the left-looking updates, 2 the diagonal-block inverses, 3 the forward/back substitution.
+// arithmetic, 1 the left-looking updates, 2 the diagonal-block inverses, 3 the forward/back substitution; inside the
+// panel: 4 the M = L L_cc^{-1} solve, 5 the rank-1 updates except of the next column, 6 the pivot reciprocals.
 #ifndef PODP_LL_ABLATE
 #define PODP_LL_ABLATE 0
 #endif
@@ -63,14 +64,6 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-// IEEE-safe complex reciprocal for pivots whose |z|^2 is outside the fast path's normal range
-__device__ __noinline__ double2 crecip_slow(double2 z) {
-  const double m = fmax(fabs(z.x), fabs(z.y));
-  const double zx = z.x / m, zy = z.y / m;
-  const double inv = 1.0 / (fma(zx, zx, zy * zy) * m);
-  return make_double2(zx * inv, -zy * inv);
 }
 
 // B fragment (k = 4s + lane%4, n = lane/4) of an 8x8 tile held as C fragments (row lane/4, cols 2(lane%4) + {0,1})
@@ -200,7 +193,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
       const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - (pos[m] & 127));
       // candidates: every remaining row (partial pivoting) or only the row at position kr (PODP_FLAG_NO_PIVOT)
       if ((PIVOT ? pos[m] >= kr : pos[m] == kr) && pos[m] < R && kk > key) key = kk;
-      rcm[m] = crecip_fast(pn[m][j]);  // speculative: off the chain after the argmax
+      if constexpr (PODP_LL_ABLATE & 64) rcm[m] = make_double2(1.0, 0.0);
+      else rcm[m] = crecip_fast(pn[m][j]);  // speculative: off the chain after the argmax
     }
     const unsigned best = __reduce_max_sync(0xffffffffu, key);
     if ((best >> 7) == 0u) return kr + 1;
@@ -209,7 +203,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     for (int m = 0; m < MSE; ++m) {
       if (pos[m] == p) {
         const double d = fma(pn[m][j].x, pn[m][j].x, pn[m][j].y * pn[m][j].y);
-        sRow[8] = (d >= 1e-290 && d <= 1e290) ? rcm[m] : crecip_slow(pn[m][j]);
+        sRow[8] = (d >= 1e-290 && d <= 1e290) ? rcm[m] : crecip_scaled(pn[m][j]);  // call-free slow path
 #pragma unroll
         for (int k = j + 1; k < 8; ++k) sRow[k] = pn[m][k];
       }
@@ -230,7 +224,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
       const double2 l = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
       if (act) pn[m][j] = l;
 #pragma unroll
-      for (int k = j + 1; k < 8; ++k) pn[m][k] = cfms(l, u[k], pn[m][k]);
+      for (int k = j + 1; k < 8; ++k)
+        if (!(PODP_LL_ABLATE & 32) || k == j + 1) pn[m][k] = cfms(l, u[k], pn[m][k]);
     }
     __syncwarp();  // sRow is rewritten by the next column
   }
@@ -252,7 +247,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
       for (int jj = k + 1; jj < 8; ++jj) {
         const double2 L = St[jj * 8 + (k ^ swz(jj))];
 #pragma unroll
-        for (int m = 0; m < MSE; ++m) pn[m][k] = cfms(pn[m][jj], L, pn[m][k]);
+        for (int m = 0; m < MSE; ++m)
+          if constexpr (!(PODP_LL_ABLATE & 16)) pn[m][k] = cfms(pn[m][jj], L, pn[m][k]);
       }
     }
 #pragma unroll
@@ -314,9 +310,14 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
   double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
 
+  // (obj, f) of evaluation t, advanced incrementally (no 64-bit division, whose subroutine call forces spills)
+  int obj = 0;
+  int64_t f = gw;
+  while (f >= a.F) {
+    f -= a.F;
+    ++obj;
+  }
   for (int64_t t = gw; t < total; t += nw) {
-    const int obj = (int)(t / a.F);
-    const int64_t f = t - (int64_t)obj * a.F;
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
@@ -474,6 +475,11 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
     }
     if (a.info && lane == 0) a.info[t] = info;
     __syncwarp();
+    f += nw;
+    while (f >= a.F) {
+      f -= a.F;
+      ++obj;
+    }
   }
 }
 

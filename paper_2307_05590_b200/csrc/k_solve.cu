@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(NW * 32) solve_smem_kernel(EvalArgs a, double2
         const double2 d = A[k * LD + k];
         if (d.x == 0.0 && d.y == 0.0) { info = k + 1; break; }
       }
-      const double2 rc = crecip(A[k * LD + k]);
+      const double2 rc = crecip_scaled(A[k * LD + k]);  // range-safe (no |p|^2 under/overflow)
       for (int i = k + 1 + lane; i < R; i += 32) A[i * LD + k] = cmul(A[i * LD + k], rc);
       __syncwarp();
       const int nr = R - k - 1, nc = R + 3 - k - 1;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(NW * 32) solve_smem_kernel(EvalArgs a, double2
     // back substitution U x = y (3 right-hand sides in columns R..R+2)
     if (info == 0) {
       for (int k = R - 1; k >= 0; --k) {
-        const double2 rc = crecip(A[k * LD + k]);
+        const double2 rc = crecip_scaled(A[k * LD + k]);  // range-safe (no |p|^2 under/overflow)
         __syncwarp();
         if (lane < 3) A[k * LD + R + lane] = cmul(A[k * LD + R + lane], rc);
         __syncwarp();

@@ -84,7 +84,9 @@ __device__ __forceinline__ int factor_panel(double2 *A, double2 *sRinv, int *sOr
     }
 #pragma unroll
     for (int m = 0; m < MS; ++m) pos[m] = (m == ms && lane == src) ? kr : (pos[m] == kr ? p : pos[m]);
-    const double2 rc = crecip_fast(pv);
+    // pivots with |p|^2 outside the normal range take the call-free scaled reciprocal (uniform branch)
+    const double pd = fma(pv.x, pv.x, pv.y * pv.y);
+    const double2 rc = (pd >= 1e-290 && pd <= 1e290) ? crecip_fast(pv) : crecip_scaled(pv);
     if (lane == 0) sRinv[kr] = rc;
 #pragma unroll
     for (int m = 0; m < MS; ++m) {

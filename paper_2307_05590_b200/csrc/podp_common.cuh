@@ -45,6 +45,21 @@ __device__ __forceinline__ double2 crecip_fast(double2 z) {
   const double inv = rcp_nr(fma(z.x, z.x, z.y * z.y));
   return make_double2(z.x * inv, -z.y * inv);
 }
+// 1/z for any finite nonzero z without a division or a call: z is scaled by the exact power of two 2^(1023-E)
+// (E = biased exponent of max(|Re|,|Im|), clamped to 2045) into max(|Re|,|Im|) in [1, 2) (or a smaller normal
+// value when z is subnormal), so |z'|^2 is a normal number for rcp_nr, and the scale is applied once more to the
+// result: 1/z = conj(z') / |z'|^2 * 2^(1023-E).  Overflows to inf only when 1/|z| is not representable (as the
+// IEEE quotient would).  Used where crecip_fast's |z|^2 leaves the normal range.
+__device__ __forceinline__ double2 crecip_scaled(double2 z) {
+  const unsigned hx = (unsigned)(__double_as_longlong(z.x) >> 32) & 0x7FF00000u;
+  const unsigned hy = (unsigned)(__double_as_longlong(z.y) >> 32) & 0x7FF00000u;
+  const unsigned h = min(hx > hy ? hx : hy, 0x7FD00000u);  // E << 20, E <= 2045
+  const double sc = __hiloint2double((int)(0x7FE00000u - h), 0);  // 2^(1023 - E), exact
+  const double zx = z.x * sc, zy = z.y * sc;
+  const double inv = rcp_nr(fma(zx, zx, zy * zy));
+  return make_double2(zx * inv * sc, -zy * inv * sc);
+}
+
 // Pivot magnitude key: max(|Re|, |Im|) from the high words of the doubles (sign cleared), i.e. exponent + top
 // 20 mantissa bits, computed on the integer pipe.  Monotone in max(|Re|,|Im|) up to 2^-20 relative.
 __device__ __forceinline__ unsigned mag_key_hi(double2 z) {

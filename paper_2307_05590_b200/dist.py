@@ -66,6 +66,22 @@ def local_interval_maxima_gpu(ev, omega_d, delta_d, snap, global_offset: int):
         w = om[i]
         n = max(k for k in range(n_int) if s[k] <= w)
         arg[n] = int(i) + global_offset
+    # an interval whose Lambda_n is exactly 0 is not returned by the theta = 1e-300 call above (0 < theta * Lambda);
+    # its argmax is its lowest candidate grid index (all entries 0; NaN ignored), found here so lam and arg agree
+    missing = [n for n in range(n_int) if lam[n] is not None and arg[n] is None]
+    if missing:
+        import numpy as np
+        dmax = np.nanmax(delta_d.cpu().numpy(), axis=1)
+        snapset = set(s)
+        for n in missing:
+            last = n == n_int - 1
+            for i, w in enumerate(om):
+                inside = s[n] <= w and (w < s[n + 1] or (last and w <= s[n + 1]))
+                if inside and w not in snapset and dmax[i] == lam[n]:
+                    arg[n] = int(i) + global_offset
+                    break
+            if arg[n] is None:  # pragma: no cover - cannot happen when lam[n] is a maximum over the interval
+                lam[n] = None
     return lam, arg
 
 

@@ -68,3 +68,27 @@ def test_shard_range_covers():
             parts = [pd.shard_range(n, w, r) for r in range(w)]
             assert parts[0][0] == 0 and parts[-1][1] == n
             assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+
+
+@pytest.mark.gpu
+def test_local_interval_maxima_zero_interval(torch_cuda):
+    """an interval whose Lambda_n is exactly 0 must come back with a consistent (lam, arg) pair."""
+    torch = torch_cuda
+    import numpy as np
+    import podp_inputs as g
+    from paper_2307_05590_b200 import Evaluator
+    from paper_2307_05590_b200.dist import local_interval_maxima_gpu
+    ev = Evaluator(g.make_operators(8))
+    om = g.omega_grid(100)
+    snap = g.snapshot_grid(5)
+    D = np.random.default_rng(0).uniform(0.5, 1.0, (100, 6))
+    D[(om >= snap[1]) & (om < snap[2])] = 0.0          # interval 1: all zero
+    lam, arg = local_interval_maxima_gpu(ev, torch.tensor(om, device="cuda"), torch.tensor(D, device="cuda"),
+                                         snap, global_offset=1000)
+    assert lam[1] == 0.0 and arg[1] is not None
+    i = arg[1] - 1000
+    assert snap[1] <= om[i] < snap[2] and om[i] not in set(snap)
+    assert i == min(j for j in range(100) if snap[1] <= om[j] < snap[2] and om[j] not in set(snap))
+    for n in range(4):
+        assert (lam[n] is None) == (arg[n] is None)
+    ev.close()

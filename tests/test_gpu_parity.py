@@ -489,3 +489,27 @@ def test_lu_kernels_deterministic_across_launch_shapes(torch_cuda, r):
             cur = torch.cat([out["T1"][0], out["I"][0], out["Delta"][0]], dim=1).cpu().numpy()
             assert np.array_equal(ref[sl].view(np.uint64), cur.view(np.uint64)), (name, sl)
     ev.close()
+
+
+@pytest.mark.parametrize("sigma", [1e-160, 1e155])
+def test_tiny_and_huge_pivots(torch_cuda, sigma):
+    """Pivots whose |p|^2 leaves the normal double range (|p| ~ 1e-160 or 1e155): every LU kernel takes its
+    call-free scaled reciprocal there (the fast reciprocal alone would return NaN rows with info = 0).
+    K, M and b0, b1 scaled by sigma (K_R = the unscaled K) leave P, R and Delta unchanged in exact arithmetic, so they
+    are gated against the oracle on the UNSCALED problem (I is not: its nu p^H M p term scales with sigma)."""
+    from paper_2307_05590_b200 import FLAG_OUT_R
+    for r in (8, 48, 96):
+        o = g.make_operators(r)
+        ops = g.Operators(**{**o.__dict__, "K": o.K * sigma, "M": o.M * sigma, "K_R": o.K.copy(),
+                             "b0": o.b0 * sigma, "b1": o.b1 * sigma})
+        omega = g.omega_grid(41)
+        for name, fl in _lu_flags(r):
+            res = run_gpu(torch_cuda, ops, omega, flags=FLAG_OUT_R | fl, want_P=True)
+            assert (res["info"] == 0).all(), (r, name)
+            for f, w in enumerate(omega):
+                w = float(w)
+                ora = oracle.evaluate_one(o, w, out_R=True)
+                assert np.linalg.norm(res["P"][0, f].T - ora["P"]) <= 1e-10 * np.linalg.norm(ora["P"]), (r, name)
+                eR, _eI, eD = errors(o, w, res["T1"][0, f], oracle.to6(ora["I"]), res["Delta"][0, f],
+                                     oracle.to6(ora["R"]), oracle.to6(ora["I"]), oracle.to6(ora["Delta"]))
+                assert eR.max() <= TOL_RI and eD.max() <= TOL_DELTA, (r, name, w)
