@@ -387,6 +387,43 @@ def main():
                     "certificate in pencil coordinates); NEXT row N3, not the LU headline"}
     except Exception as exc:  # pragma: no cover
         variants["pencil_N3"] = {"error": str(exc)[:200]}
+    # NEXT row N1: the literal per-direction form (three LU solves of size M_i per omega + cross-block contractions)
+    # against the block-diagonal embedding of size sum M_i, on the same synthetic blocks and the step's omegas
+    try:
+        from paper_2307_05590_b200 import perdir as pdir
+        res_n1 = {}
+        for mm in ((16, 16, 16), (24, 16, 8)):
+            blk = g.make_perdir_blocks(mm)
+            ev_lit = pb.Evaluator.per_direction(blk["Kb"], blk["Cb"], blk["b0"], blk["b1"], blk["Hb"], blk["N0"],
+                                                blk["S"], blk["Gx"], blk["nu"], blk["alpha"], blk["alpha_lb"],
+                                                device=local)
+            ev_emb = pb.Evaluator(pdir.embed(blk["Kb"], blk["Cb"], blk["b0"], blk["b1"], blk["Hb"], blk["N0"],
+                                             blk["S"], blk["Gx"], blk["nu"], blk["alpha"], blk["alpha_lb"]),
+                                  device=local)
+            row = {}
+            for name, evx in (("literal", ev_lit), ("embedding", ev_emb)):
+                for _ in range(args.warmup):
+                    evx.eval(w_d, out=out)
+                torch.cuda.synchronize()
+                ms = 0.0
+                for _ in range(args.steps):
+                    flush.zero_()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    evx.eval(w_d, out=out)
+                    e1.record(stream)
+                    e1.synchronize()
+                    ms += e0.elapsed_time(e1)
+                row[name] = {"value": F * args.steps / (ms / 1e3), "unit": UNIT, "ms_per_eval": ms / args.steps}
+                evx.close()
+            row["speedup_literal"] = row["embedding"]["ms_per_eval"] / row["literal"]["ms_per_eval"]
+            res_n1["M=" + "+".join(str(x) for x in mm)] = row
+        variants["perdir_N1"] = dict(res_n1, note="podp_eval only (no select); literal = podp_create_perdir "
+                                                  "(3 batched LU solves of size M_i + placement + contraction), "
+                                                  "embedding = one LU of size sum M_i (block-diagonal K, M)")
+    except Exception as exc:  # pragma: no cover
+        variants["perdir_N1"] = {"error": str(exc)[:200]}
     # NEXT row N2: one Algorithm-1 run (off-line cuSOLVER/cuBLAS + on-line libpodp certification on a 1e5 grid)
     if rank == 0 and not args.no_adapt:
         try:

@@ -105,6 +105,35 @@ podp_status podp_create(const podp_operators *ops, int device, void *cuda_stream
 podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int device, void *cuda_stream,
                               podp_ctx **out);
 
+/* NEXT row N1 in the paper's LITERAL per-direction form (P:584 U_i^M per direction with M_i modes; P:593-596
+ * eqn:ReducedA, one reduced system A_i^M p_i = r_i^M of size M_i per direction; P:600-604 eqn:podprealmpt and
+ * P:606-620 eqn:podpimagmpt with the rectangular cross blocks K_ij^M, C_ij^M, h_i^(j); P:651-661 the certificate
+ * from the direction Grams G_ij = W_i^H W_j, W_i = [B0_i, B1_i | K U_i | M U_i]).  All pointers host, complex =
+ * interleaved (re, im) doubles, row-major; copied by podp_create_perdir; caller keeps ownership. */
+typedef struct {
+  int32_t m[3];         /* M_1, M_2, M_3 >= 1 with M_1 + M_2 + M_3 <= PODP_R_MAX                                 */
+  double nu, alpha, alpha_lb;                   /* as in podp_operators                                          */
+  const double *K[9];   /* K[3i+j]: M_i x M_j complex, K_ij^M = U_i^H K U_j; K[3i+i] Hermitian (the direction-i
+                           system stiffness); all nine blocks enter R_ij                          */
+  const double *C[9];   /* C[3i+j]: M_i x M_j complex, C_ij^M / nu = U_i^H M U_j; C[3i+i] Hermitian PSD (the
+                           direction-i conductor mass); all nine enter I_ij                       */
+  const double *b0[3];  /* b0[i]: M_i complex, omega^0 part of r_i^M (reading U2)                                */
+  const double *b1[3];  /* b1[i]: M_i complex, omega^1 part                                                       */
+  const double *H[9];   /* H[3i+j]: M_j complex, row h_i^(j) = o_i^T C2 U_j + t_i U_j (unconjugated)       */
+  const double *N0;     /* 3 x 3 real symmetric                                                                  */
+  const double *S;      /* 3 x 3 real symmetric                                                      */
+  const double *G[9];   /* G[3i+j]: (2+2M_i) x (2+2M_j) complex, W_i^H W_j with W_i's slot order
+                           [B0_i, B1_i | K U_i (M_i) | M U_i (M_i)]; G[3i+j] = G[3j+i]^H                        */
+} podp_perdir_operators;
+
+/* Validate + pack the literal per-direction operators.  podp_eval on the returned context solves the THREE
+ * direction systems (sizes M_1, M_2, M_3: three batched LU solves per omega instead of one of size sum M_i) and
+ * evaluates R, I and Delta from the cross blocks; outputs, info (k+1 for a zero pivot at step k of the
+ * concatenated columns, i.e. M_1 + ... + M_{i-1} + k_i + 1 for direction i) and podp_select are as for podp_eval,
+ * and PODP_FLAG_OUT_P returns P as 3 x (M_1+M_2+M_3) with column i = (0, p_i^M, 0).  PODP_FLAG_PENCIL is
+ * PODP_ERR_UNSUPPORTED on such a context.  Errors as podp_create. */
+podp_status podp_create_perdir(const podp_perdir_operators *ops, int device, void *cuda_stream, podp_ctx **out);
+
 /* Device-buffer evaluation (the hot path).  Asynchronous on cuda_stream; no host synchronisation.
  *   omega_d : device, F doubles (the same output grid for every object)
  *   T1_d    : device, n_obj x F x 6 doubles: Rt = N0 + R (default) or R (PODP_FLAG_OUT_R)

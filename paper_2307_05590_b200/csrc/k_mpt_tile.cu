@@ -36,7 +36,12 @@ struct Cfg {
 // DIAG (N3 pencil coordinates with K_R = K and M_I = M): Z^H K Z = I and Z^H M Z = Lambda, so the K_R and M_I
 // quadratic forms are diagonal -- Re(y_i^H y_j) and Re(y_i^H Lambda y_j) -- and are accumulated in the slice pass;
 // only Q~ = Z^H Q Z stays dense.
-template <int R, bool DIAG>
+// BLK (N1 literal per-direction form): column i of P is nonzero only in direction block i (rows
+// [a.blk_lo[i], a.blk_hi[i]), SL-aligned), so for an operator row a in block i only the pairs (i, j >= i) get a
+// contribution, y_j[a] runs only over block j, and those are exactly the rectangular cross blocks K_ij^M, C_ij^M
+// and the Gram blocks of eqn:podprealmpt / eqn:podpimagmpt and P:651-661.  Skipped terms are exact
+// zeros, so the sums equal the dense ones bit for bit (for finite operators).
+template <int R, bool DIAG, bool BLK = false>
 __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalArgs a) {
   using C = mpttile::Cfg<R>;
   constexpr int NBL = C::NBL, RB = C::RB, NBLK = C::NBLK, LD = C::LD, SL = C::SL, TILE = C::TILE, FPW = C::FPW;
@@ -160,6 +165,8 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
 #pragma unroll 1
       for (int ar = a0; ar < a1; ++ar) {
         const int row = (ar - a0) * ld;
+        // BLK: block of this operator row (warp-uniform); only pairs (cb, j >= cb) receive contributions
+        const int cb = BLK ? (ar < a.blk_hi[0] ? 0 : (ar < a.blk_hi[1] ? 1 : 2)) : 0;
         double2 pa[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) pa[c] = __ldg(Pw + c * R + ar);
@@ -169,7 +176,32 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
 #pragma unroll
         for (int tt = 0; tt < NBL; ++tt) {
           const int b = sl + SL * tt;
-          if ((R % SL) == 0 || b < R) {
+          if constexpr (BLK) {
+            // b-group [SL tt, SL tt + SL) lies in one block gb (blocks are SL-aligned): only column gb is nonzero
+            // there, and it is needed only if gb >= cb
+            const int gb = SL * tt < a.blk_hi[0] ? 0 : (SL * tt < a.blk_hi[1] ? 1 : 2);
+            if (gb < cb) continue;
+            const double2 gk = oGk[row + b], jj = oJ[row + b], gm = oGm[row + b];
+            const double2 q = make_double2(fma(s, fma(s, gm.x, jj.x), gk.x), fma(s, fma(s, gm.y, jj.y), gk.y));
+            const double2 kr = oKR[row + b], mm = oM[row + b];
+            switch (gb) {
+              case 0:
+                yK[0] = cfma(kr, p[tt][0], yK[0]);
+                yM[0] = cfma(mm, p[tt][0], yM[0]);
+                yQ[0] = cfma(q, p[tt][0], yQ[0]);
+                break;
+              case 1:
+                yK[1] = cfma(kr, p[tt][1], yK[1]);
+                yM[1] = cfma(mm, p[tt][1], yM[1]);
+                yQ[1] = cfma(q, p[tt][1], yQ[1]);
+                break;
+              default:
+                yK[2] = cfma(kr, p[tt][2], yK[2]);
+                yM[2] = cfma(mm, p[tt][2], yM[2]);
+                yQ[2] = cfma(q, p[tt][2], yQ[2]);
+                break;
+            }
+          } else if ((R % SL) == 0 || b < R) {
             const double2 gk = oGk[row + b], jj = oJ[row + b], gm = oGm[row + b];
             const double2 q = make_double2(fma(s, fma(s, gm.x, jj.x), gk.x), fma(s, fma(s, gm.y, jj.y), gk.y));
             if constexpr (!DIAG) {
@@ -188,6 +220,7 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
         for (int e = 0; e < 6; ++e) {
           const int i = e < 3 ? e : (e < 5 ? 0 : 1);
           const int j = e < 3 ? e : (e == 3 ? 1 : 2);
+          if (BLK && i != cb) continue;  // conj(p_i[a]) = 0 outside block i
           if constexpr (!DIAG) {
             qK[e] = fma(pa[i].x, yK[j].x, fma(pa[i].y, yK[j].y, qK[e]));
             qM[e] = fma(pa[i].x, yM[j].x, fma(pa[i].y, yM[j].y, qM[e]));
@@ -266,7 +299,8 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
 template <int R>
 static cudaError_t launch_mpt_tile_t(const EvalArgs &a, cudaStream_t s, bool diag) {
   using C = mpttile::Cfg<R>;
-  auto kern = diag ? mpt_tile_kernel<R, true> : mpt_tile_kernel<R, false>;
+  auto kern = a.blk_hi[0] > 0 ? mpt_tile_kernel<R, false, true>
+                              : (diag ? mpt_tile_kernel<R, true> : mpt_tile_kernel<R, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;

@@ -26,6 +26,12 @@ struct podp_ctx {
   bool pencil_done = false;
   bool pencil_ok = false;    // K positive definite for every object
   bool pencil_diag = false;  // every object has K_R = K and M_I = M: Z^H K_R Z = I, Z^H M_I Z = Lambda exactly
+  // N1 literal per-direction form (podp_create_perdir): this context holds the concatenated cross-block operators
+  // used by the contraction kernel; dir[i] holds direction i's system (M_i modes, padded to 8 ceil(M_i / 8)),
+  // factored by its own solve launch
+  podp_ctx *dir[3] = {nullptr, nullptr, nullptr};
+  int m[3] = {0, 0, 0};
+  int offp[3] = {0, 0, 0};  // direction block offsets in the padded (SL-aligned) concatenation
 };
 
 namespace {
@@ -493,6 +499,8 @@ int32_t podp_profile_read(char *names, double *ms, int64_t *counts, int32_t max_
 
 podp_status podp_destroy(podp_ctx *c) {
   if (!c) return PODP_OK;
+  for (int i = 0; i < 3; ++i)
+    if (c->dir[i]) podp_destroy(c->dir[i]);
   DeviceGuard guard(c->device);
   cudaDeviceSynchronize();
   cudaFree(c->d_ops);
@@ -500,6 +508,136 @@ podp_status podp_destroy(podp_ctx *c) {
   delete c;
   return PODP_OK;
 }
+
+}  // extern "C"
+
+namespace {
+
+enum SolverKind { K_LL, K_BLK, K_DYN, K_GEN, K_PENCIL };
+
+// Solver for padded size R: the one-warp left-looking kernel for R <= 64, the blocked multi-warp kernels (measured
+// table) up to 96, the generic kernel beyond (and for NO_PIVOT above 64); PODP_FLAG_LU_* overrides (A/B).
+podp_status pick_solver(int R, int flags, SolverKind *ker) {
+  const int lu_sel = flags & (PODP_FLAG_LU_LL | PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC);
+  if (lu_sel & (lu_sel - 1)) return fail(PODP_ERR_ARG, "at most one PODP_FLAG_LU_* solver may be requested");
+  if ((lu_sel == PODP_FLAG_LU_LL && R > 64) || ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && R > 96))
+    return fail(PODP_ERR_UNSUPPORTED, "requested LU kernel is not instantiated for padded r = %d", R);
+  if ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && (flags & PODP_FLAG_NO_PIVOT))
+    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_LU_BLK / _DYN always pivot");
+  if (flags & PODP_FLAG_PENCIL) *ker = K_PENCIL;
+  else if (lu_sel == PODP_FLAG_LU_LL) *ker = K_LL;
+  else if (lu_sel == PODP_FLAG_LU_BLK) *ker = K_BLK;
+  else if (lu_sel == PODP_FLAG_LU_DYN) *ker = K_DYN;
+  else if (lu_sel == PODP_FLAG_LU_GENERIC) *ker = K_GEN;
+  else if (R <= 64) *ker = K_LL;
+  else if (flags & PODP_FLAG_NO_PIVOT) *ker = K_GEN;
+  else if (R <= 96) *ker = (R == 72 || R >= 80) ? K_DYN : K_BLK;
+  else *ker = K_GEN;
+  return PODP_OK;
+}
+
+size_t solver_scratch_bytes(SolverKind ker, int R, int sms) {
+  if (ker == K_LL) return podp::lu_ll_scratch_bytes(R, sms);
+  if (ker == K_DYN) return podp::lu_dyn_scratch_bytes(R, sms);
+  if (ker == K_GEN) return podp::solve_scratch_bytes(R, sms);
+  return 0;
+}
+
+cudaError_t launch_solver(SolverKind ker, const podp::EvalArgs &a, cudaStream_t s, int sms, bool pencil_y) {
+  switch (ker) {
+    case K_PENCIL: return pencil_y ? podp::launch_pencil_y(a, s) : podp::launch_pencil(a, s);
+    case K_LL: return podp::launch_lu_ll(a, s, sms);
+    case K_BLK: return podp::launch_lu_blk(a, s);
+    case K_DYN: return podp::launch_lu_dyn(a, s);
+    case K_GEN: return podp::launch_solve(a, s, a.gscr);
+  }
+  return cudaErrorInvalidValue;
+}
+
+podp::EvalArgs make_args(const podp_ctx *c, const double *omega_d, int64_t F, double *T1_d, double *I_d,
+                         double *Delta_d, int32_t *info_d, double *P_out, int flags) {
+  podp::EvalArgs a;
+  a.ops = c->d_ops;
+  a.L = c->L;
+  a.r = c->r;
+  a.n_obj = c->n_obj;
+  a.omega = omega_d;
+  a.F = F;
+  a.T1 = T1_d;
+  a.I = I_d;
+  a.Delta = Delta_d;
+  a.info = info_d;
+  a.P_out = P_out;
+  a.flags = flags;
+  a.Pws = nullptr;
+  a.gscr = nullptr;
+  a.blk_hi[0] = a.blk_hi[1] = 0;
+  return a;
+}
+
+// N1 literal form: three direction solves (batch of 3 objects of padded size R_s) -> placement into the
+// concatenated columns -> the contraction kernel with the cross-block operators of this context.
+podp_status eval_perdir(podp_ctx *c, const double *omega_d, int64_t F, double *T1_d, double *I_d, double *Delta_d,
+                        int32_t *info_d, double *P_d, int flags, cudaStream_t s) {
+  if (flags & PODP_FLAG_PENCIL) return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_PENCIL on a per-direction context");
+  const int Re = c->L.R;
+  SolverKind ker[3];
+  int Rs[3];
+  size_t p3[3], gsz[3], total = 0;
+  for (int i = 0; i < 3; ++i) {
+    Rs[i] = c->dir[i]->L.R;
+    podp_status st = pick_solver(Rs[i], flags, &ker[i]);
+    if (st != PODP_OK) return st;
+    p3[i] = (size_t)F * 3 * Rs[i] * sizeof(double2);
+    gsz[i] = (solver_scratch_bytes(ker[i], Rs[i], c->sms) + 255) / 256 * 256;
+    total += p3[i] + gsz[i];
+  }
+  const size_t pe = (size_t)F * 3 * Re * sizeof(double2);
+  const size_t in3 = (((size_t)3 * F * sizeof(int32_t)) + 255) / 256 * 256;
+  char *buf = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync((void **)&buf, total + pe + in3, c->pool, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(per-direction workspace)");
+  double2 *Pe = reinterpret_cast<double2 *>(buf);
+  int32_t *info3 = reinterpret_cast<int32_t *>(buf + pe);
+  const double2 *Pd[3];
+  int nl = 0;
+  size_t at = pe + in3;
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i) {
+    podp::EvalArgs ai = make_args(c->dir[i], omega_d, F, nullptr, nullptr, nullptr, info3 + (size_t)i * F, nullptr,
+                                  flags & ~(PODP_FLAG_OUT_P));
+    ai.Pws = reinterpret_cast<double2 *>(buf + at);
+    Pd[i] = ai.Pws;
+    at += p3[i];
+    ai.gscr = gsz[i] ? reinterpret_cast<double2 *>(buf + at) : nullptr;
+    at += gsz[i];
+    ProfScope ps("solve", s);
+    e = launch_solver(ker[i], ai, s, c->sms, false);
+    if (e == cudaSuccess) ++nl;
+  }
+  if (e == cudaSuccess) {
+    ProfScope ps("scatter", s);
+    e = podp::launch_perdir_scatter(Pd, Rs, c->m, c->offp, info3, F, Pe, Re, info_d,
+                                    (flags & PODP_FLAG_OUT_P) ? P_d : nullptr, s);
+    if (e == cudaSuccess) ++nl;
+  }
+  if (e == cudaSuccess) {
+    podp::EvalArgs am = make_args(c, omega_d, F, T1_d, I_d, Delta_d, nullptr, nullptr, flags);
+    am.Pws = Pe;
+    am.blk_hi[0] = c->offp[1];
+    am.blk_hi[1] = c->offp[2];
+    ProfScope ps("mpt", s);
+    e = podp::launch_mpt_tile(am, s, false);
+    if (e == cudaSuccess) ++nl;
+  }
+  cudaFreeAsync(buf, s);
+  g_last_launches = nl;
+  if (e != cudaSuccess) return cuda_fail(e, "podp_eval (per-direction) launch");
+  return PODP_OK;
+}
+
+}  // namespace
+
+extern "C" {
 
 podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, double *T1_d, double *I_d,
                       double *Delta_d, int32_t *info_d, double *P_d, int flags, void *cuda_stream) {
@@ -514,16 +652,14 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
   const int known = PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_FLAG_PENCIL | PODP_FLAG_LU_LL |
                     PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC;
   if (flags & ~known) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
-  const int lu_sel = flags & (PODP_FLAG_LU_LL | PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC);
-  if (lu_sel & (lu_sel - 1)) return fail(PODP_ERR_ARG, "at most one PODP_FLAG_LU_* solver may be requested");
-  const int R = c->L.R;
-  if ((lu_sel == PODP_FLAG_LU_LL && R > 64) || ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && R > 96))
-    return fail(PODP_ERR_UNSUPPORTED, "requested LU kernel is not instantiated for padded r = %d", R);
-  if ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && (flags & PODP_FLAG_NO_PIVOT))
-    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_LU_BLK / _DYN always pivot");
   DeviceGuard guard(c->device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (c->dir[0]) return eval_perdir(c, omega_d, F, T1_d, I_d, Delta_d, info_d, P_d, flags, s);
+  const int R = c->L.R;
+  SolverKind ker;
+  podp_status st0 = pick_solver(R, flags, &ker);
+  if (st0 != PODP_OK) return st0;
   if (flags & PODP_FLAG_PENCIL) {
     std::lock_guard<std::mutex> lk(c->pencil_mu);
     if (!c->pencil_done) {
@@ -533,37 +669,9 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
     if (!c->pencil_ok)
       return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_PENCIL needs K Hermitian positive definite (Cholesky failed)");
   }
-  // solver: the one-warp left-looking kernel for R <= 64, the blocked multi-warp kernels (measured table) up to 96,
-  // the generic kernel beyond (and for NO_PIVOT above 64)
-  enum { K_LL, K_BLK, K_DYN, K_GEN, K_PENCIL } ker;
-  if (flags & PODP_FLAG_PENCIL) ker = K_PENCIL;
-  else if (lu_sel == PODP_FLAG_LU_LL) ker = K_LL;
-  else if (lu_sel == PODP_FLAG_LU_BLK) ker = K_BLK;
-  else if (lu_sel == PODP_FLAG_LU_DYN) ker = K_DYN;
-  else if (lu_sel == PODP_FLAG_LU_GENERIC) ker = K_GEN;
-  else if (R <= 64) ker = K_LL;
-  else if (flags & PODP_FLAG_NO_PIVOT) ker = K_GEN;
-  else if (R <= 96) ker = (R == 72 || R >= 80) ? K_DYN : K_BLK;
-  else ker = K_GEN;
-  podp::EvalArgs a;
-  a.ops = c->d_ops;
-  a.L = c->L;
-  a.r = c->r;
-  a.n_obj = c->n_obj;
-  a.omega = omega_d;
-  a.F = F;
-  a.T1 = T1_d;
-  a.I = I_d;
-  a.Delta = Delta_d;
-  a.info = info_d;
-  a.P_out = (flags & PODP_FLAG_OUT_P) ? P_d : nullptr;
-  a.flags = flags;
-  a.Pws = nullptr;
-  a.gscr = nullptr;
-  size_t gsz = 0;
-  if (ker == K_LL) gsz = podp::lu_ll_scratch_bytes(R, c->sms);
-  else if (ker == K_DYN) gsz = podp::lu_dyn_scratch_bytes(R, c->sms);
-  else if (ker == K_GEN) gsz = podp::solve_scratch_bytes(R, c->sms);
+  podp::EvalArgs a = make_args(c, omega_d, F, T1_d, I_d, Delta_d, info_d,
+                               (flags & PODP_FLAG_OUT_P) ? P_d : nullptr, flags);
+  const size_t gsz = solver_scratch_bytes(ker, R, c->sms);
   const size_t ws = (size_t)c->n_obj * (size_t)F * 3 * R * sizeof(double2);
   cudaError_t e = cudaMallocFromPoolAsync((void **)&a.Pws, ws, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(P workspace)");
@@ -590,13 +698,7 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
   }
   {
     ProfScope ps("solve", s);
-    switch (ker) {
-      case K_PENCIL: e = pencil_y ? podp::launch_pencil_y(a, s) : podp::launch_pencil(a, s); break;
-      case K_LL: e = podp::launch_lu_ll(a, s, c->sms); break;
-      case K_BLK: e = podp::launch_lu_blk(a, s); break;
-      case K_DYN: e = podp::launch_lu_dyn(a, s); break;
-      case K_GEN: e = podp::launch_solve(a, s, a.gscr); break;
-    }
+    e = launch_solver(ker, a, s, c->sms, pencil_y);
     if (e == cudaSuccess) ++nl;
   }
   if (e == cudaSuccess) {
@@ -701,6 +803,130 @@ podp_status podp_select(const podp_ctx *c, const double *omega_d, const double *
     idx_new[q] = q < nc ? (int64_t)res[2 + n_int + q] : -1;
     omega_new[q] = q < nc ? res[2 + n_int + n_star + q] : std::nan("");
   }
+  return PODP_OK;
+}
+
+podp_status podp_create_perdir(const podp_perdir_operators *o, int device, void *cuda_stream, podp_ctx **out) {
+  g_err.clear();
+  if (!out) return fail(PODP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!o) return fail(PODP_ERR_ARG, "ops is NULL");
+  int off[4] = {0, 0, 0, 0};
+  for (int i = 0; i < 3; ++i) {
+    if (o->m[i] < 1) return fail(PODP_ERR_ARG, "M_%d = %d must be >= 1", i + 1, o->m[i]);
+    off[i + 1] = off[i] + o->m[i];
+  }
+  if (off[3] > PODP_R_MAX) return fail(PODP_ERR_ARG, "M_1 + M_2 + M_3 = %d exceeds %d", off[3], PODP_R_MAX);
+  // concatenation with each direction block padded to the contraction kernel's b-slice width (8 up to 64 rows,
+  // else 16), so the kernel can skip the zero blocks per b-group; the padding rows and columns are exact zeros
+  int pad = 8, offp[4] = {0, 0, 0, 0};
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i < 3; ++i) offp[i + 1] = offp[i] + (o->m[i] + pad - 1) / pad * pad;
+    if (offp[3] <= 64) break;
+    pad = 16;
+  }
+  const int r = offp[3];
+  if (r > PODP_R_MAX)
+    return fail(PODP_ERR_UNSUPPORTED, "padded per-direction concatenation (%d) exceeds %d", r, PODP_R_MAX);
+  if (!o->N0 || !o->S) return fail(PODP_ERR_ARG, "null N0 / S");
+  for (int q = 0; q < 9; ++q)
+    if (!o->K[q] || !o->C[q] || !o->H[q] || !o->G[q]) return fail(PODP_ERR_ARG, "null block pointer (index %d)", q);
+  for (int i = 0; i < 3; ++i)
+    if (!o->b0[i] || !o->b1[i]) return fail(PODP_ERR_ARG, "null b0/b1 pointer (direction %d)", i + 1);
+  // (1) the concatenated cross-block operators for the contraction kernel (placement only): K, M block-diagonal
+  //     (unused by the solve, which runs on the direction contexts; K's padding diagonal is 1 for validity),
+  //     K_R = [K_ij], M_I = [C_ij], b column i in block i, H row i = [h_i^(j)]_j, G placed from the G_ij
+  const int ng = 6 + 2 * r;
+  std::vector<double> K((size_t)2 * r * r, 0.0), M(K.size(), 0.0), KR(K.size(), 0.0), MI(K.size(), 0.0);
+  std::vector<double> B0((size_t)6 * r, 0.0), B1(B0.size(), 0.0), H(B0.size(), 0.0), G((size_t)2 * ng * ng, 0.0);
+  for (int i = 0; i < 3; ++i)
+    for (int a = o->m[i]; a < offp[i + 1] - offp[i]; ++a) K[2 * ((size_t)(offp[i] + a) * r + offp[i] + a)] = 1.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double *Kb = o->K[3 * i + j], *Cb = o->C[3 * i + j];
+      for (int a = 0; a < o->m[i]; ++a)
+        for (int b = 0; b < o->m[j]; ++b)
+          for (int cc = 0; cc < 2; ++cc) {
+            const size_t e = 2 * ((size_t)(offp[i] + a) * r + offp[j] + b) + cc, src = 2 * ((size_t)a * o->m[j] + b) + cc;
+            KR[e] = Kb[src];
+            MI[e] = Cb[src];
+            if (i == j) {
+              K[e] = Kb[src];
+              M[e] = Cb[src];
+            }
+          }
+      for (int b = 0; b < o->m[j]; ++b)
+        for (int cc = 0; cc < 2; ++cc) H[2 * ((size_t)i * r + offp[j] + b) + cc] = o->H[3 * i + j][2 * b + cc];
+      // slot map of direction d in the stacked (6 + 2r) factor: [2d, 2d+1 | 6 + offp_d + a | 6 + r + offp_d + a]
+      auto slot = [&](int d, int a) { return a < 2 ? 2 * d + a : (a < 2 + o->m[d] ? 6 + offp[d] + (a - 2) : 6 + r + offp[d] + (a - 2 - o->m[d])); };
+      const int ni = 2 + 2 * o->m[i], nj = 2 + 2 * o->m[j];
+      for (int a = 0; a < ni; ++a)
+        for (int b = 0; b < nj; ++b)
+          for (int cc = 0; cc < 2; ++cc)
+            G[2 * ((size_t)slot(i, a) * ng + slot(j, b)) + cc] = o->G[3 * i + j][2 * ((size_t)a * nj + b) + cc];
+    }
+  for (int i = 0; i < 3; ++i)
+    for (int a = 0; a < o->m[i]; ++a)
+      for (int cc = 0; cc < 2; ++cc) {
+        B0[2 * ((size_t)(offp[i] + a) * 3 + i) + cc] = o->b0[i][2 * a + cc];
+        B1[2 * ((size_t)(offp[i] + a) * 3 + i) + cc] = o->b1[i][2 * a + cc];
+      }
+  podp_operators emb = {};
+  emb.r = r;
+  emb.nu = o->nu;
+  emb.alpha = o->alpha;
+  emb.alpha_lb = o->alpha_lb;
+  emb.K = K.data();
+  emb.M = M.data();
+  emb.K_R = KR.data();
+  emb.M_I = MI.data();
+  emb.b0 = B0.data();
+  emb.b1 = B1.data();
+  emb.N0 = o->N0;
+  emb.S = o->S;
+  emb.H = H.data();
+  emb.G = G.data();
+  podp_ctx *main_ctx = nullptr;
+  podp_status st = podp_create_batch(1, &emb, device, cuda_stream, &main_ctx);
+  if (st != PODP_OK) return st;
+  // (2) the three direction systems, each its own single-object context of size M_i (exact padding to
+  //     8 ceil(M_i / 8): K_pad = diag(K_ii, I), M_pad = diag(C_ii, 0)), right-hand side in column i; their other
+  //     operands are unused (zero)
+  for (int i = 0; i < 3; ++i) {
+    const int mi = o->m[i], ngs = 6 + 2 * mi;
+    std::vector<double> zH((size_t)6 * mi, 0.0), zG((size_t)2 * ngs * ngs, 0.0), zS(9, 0.0), eye3(9, 0.0);
+    std::vector<double> db0((size_t)6 * mi, 0.0), db1((size_t)6 * mi, 0.0);
+    eye3[0] = eye3[4] = eye3[8] = 1.0;
+    for (int a = 0; a < mi; ++a)
+      for (int cc = 0; cc < 2; ++cc) {
+        db0[2 * ((size_t)a * 3 + i) + cc] = o->b0[i][2 * a + cc];
+        db1[2 * ((size_t)a * 3 + i) + cc] = o->b1[i][2 * a + cc];
+      }
+    podp_operators d = {};
+    d.r = mi;
+    d.nu = o->nu;
+    d.alpha = o->alpha;
+    d.alpha_lb = o->alpha_lb;
+    d.K = o->K[4 * i];
+    d.M = o->C[4 * i];
+    d.b0 = db0.data();
+    d.b1 = db1.data();
+    d.N0 = eye3.data();
+    d.S = zS.data();
+    d.H = zH.data();
+    d.G = zG.data();
+    st = podp_create_batch(1, &d, device, cuda_stream, &main_ctx->dir[i]);
+    if (st != PODP_OK) {
+      podp_destroy(main_ctx);
+      return st;
+    }
+  }
+  for (int i = 0; i < 3; ++i) {
+    main_ctx->m[i] = o->m[i];
+    main_ctx->offp[i] = offp[i];
+  }
+  main_ctx->r = off[3];  // the caller's concatenated size (PODP_FLAG_OUT_P layout, podp_r)
+  *out = main_ctx;
   return PODP_OK;
 }
 

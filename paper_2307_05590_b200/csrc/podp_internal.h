@@ -41,6 +41,8 @@ struct EvalArgs {
   double2 *Pws;        // workspace: n_obj x F x 3 x R complex (solve -> contraction hand-off)
   double2 *gscr;       // LU scratch (kernel-specific size, see the *_scratch_bytes functions), nullable
   int flags;
+  int blk_hi[2];       // N1 literal form: ends of direction blocks 0 and 1 in the concatenated rows (SL-aligned);
+                       // blk_hi[0] == 0 for the shared-basis form
 };
 
 // Kernel launchers (return cudaGetLastError() after the launch; cudaErrorNotSupported if no instantiation).
@@ -60,6 +62,9 @@ bool pencil_precompute(int r, const double *K, const double *M, const double *b0
                        std::vector<double> &c1);
 cudaError_t launch_solve(const EvalArgs &a, cudaStream_t s, double2 *gscratch);  // generic: any R, pivot or not
 size_t solve_scratch_bytes(int R, int sms);  // global scratch launch_solve needs for this R (0 if shared fits)
+cudaError_t launch_perdir_scatter(const double2 *const Pd[3], const int Rs[3], const int m[3], const int offp[3],
+                                  const int32_t *info3, int64_t F, double2 *Pe, int Re, int32_t *info, double *P_out,
+                                  cudaStream_t s);
 cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, const double *snap_d, int n_snap,
                           int n_star, double theta, unsigned long long *lam_bits, unsigned long long *arg_idx,
                           double *result_d, cudaStream_t s, int *nlaunch);

@@ -28,7 +28,7 @@ FLAG_LU_GENERIC = 1 << 11
 R_MAX = 128
 STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ERR_OOM", 4: "PODP_ERR_UNSUPPORTED",
                 5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}
-EXPORTED = ["podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
+EXPORTED = ["podp_create", "podp_create_batch", "podp_create_perdir", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
             "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version", "podp_profile_enable",
             "podp_profile_read", "podp_invariants", "podp_coil_voltage"]
 
@@ -46,6 +46,13 @@ class podp_operators(ctypes.Structure):
         (n, ctypes.POINTER(ctypes.c_double)) for n in ("K", "M", "K_R", "b0", "b1", "N0", "S", "H", "G", "M_I")]
 
 
+class podp_perdir_operators(ctypes.Structure):
+    _DP = ctypes.POINTER(ctypes.c_double)
+    _fields_ = [("m", ctypes.c_int32 * 3), ("nu", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("alpha_lb", ctypes.c_double), ("K", _DP * 9), ("C", _DP * 9), ("b0", _DP * 3), ("b1", _DP * 3),
+                ("H", _DP * 9), ("N0", _DP), ("S", _DP), ("G", _DP * 9)]
+
+
 _lib = None
 
 
@@ -61,13 +68,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     i32, i64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     lib.podp_create.argtypes = [ctypes.POINTER(podp_operators), ctypes.c_int, P, ctypes.POINTER(P)]
     lib.podp_create_batch.argtypes = [i32, ctypes.POINTER(podp_operators), ctypes.c_int, P, ctypes.POINTER(P)]
+    lib.podp_create_perdir.argtypes = [ctypes.POINTER(podp_perdir_operators), ctypes.c_int, P, ctypes.POINTER(P)]
     lib.podp_eval.argtypes = [P, P, i64, P, P, P, P, P, ctypes.c_int, P]
     lib.podp_eval_host.argtypes = [P, P, i64, P, P, P, P, ctypes.c_int, P]
     lib.podp_select.argtypes = [P, P, P, i64, P, i32, i32, dbl, P, P, P, P, P, P]
     lib.podp_n_obj.argtypes = [P]
     lib.podp_r.argtypes = [P]
     lib.podp_destroy.argtypes = [P]
-    for fn in ("podp_create", "podp_create_batch", "podp_eval", "podp_eval_host", "podp_select", "podp_destroy"):
+    for fn in ("podp_create", "podp_create_batch", "podp_create_perdir", "podp_eval", "podp_eval_host", "podp_select", "podp_destroy"):
         getattr(lib, fn).restype = ctypes.c_int
     lib.podp_n_obj.restype = i32
     lib.podp_r.restype = i32
@@ -196,6 +204,44 @@ def _stream_handle(stream):
 
 class Evaluator:
     """podp_create / podp_create_batch + podp_eval / podp_eval_host / podp_select on one device."""
+
+    @classmethod
+    def per_direction(cls, Kb, Cb, b0, b1, Hb, N0, S, Gx, nu: float, alpha: float, alpha_lb: float,
+                      device: int = 0, stream=None) -> "Evaluator":
+        """NEXT row N1, literal form (podp_create_perdir): Kb[i][j], Cb[i][j] the M_i x M_j blocks K_ij^M and
+        C_ij^M / nu; b0[i], b1[i] length M_i; Hb[i][j] the length-M_j rows h_i^(j); Gx[i][j] the direction Grams
+        W_i^H W_j ((2 + 2 M_i) x (2 + 2 M_j)).  Argument marshalling only."""
+        lib = load_library()
+        m = [int(np.asarray(b0[i]).shape[0]) for i in range(3)]
+        st = podp_perdir_operators()
+        keep: list = []
+
+        def put(a):
+            keep.append(a)
+            return _dptr(a)
+        for i in range(3):
+            st.m[i] = m[i]
+            st.b0[i] = put(_c128(b0[i], (m[i],)))
+            st.b1[i] = put(_c128(b1[i], (m[i],)))
+            for j in range(3):
+                st.K[3 * i + j] = put(_c128(Kb[i][j], (m[i], m[j])))
+                st.C[3 * i + j] = put(_c128(Cb[i][j], (m[i], m[j])))
+                st.H[3 * i + j] = put(_c128(Hb[i][j], (m[j],)))
+                st.G[3 * i + j] = put(_c128(Gx[i][j], (2 + 2 * m[i], 2 + 2 * m[j])))
+        st.N0 = put(_f64(N0, (3, 3)))
+        st.S = put(_f64(S, (3, 3)))
+        st.nu, st.alpha, st.alpha_lb = float(nu), float(alpha), float(alpha_lb)
+        h = ctypes.c_void_p()
+        import torch
+        with torch.cuda.device(device):
+            _check(lib.podp_create_perdir(ctypes.byref(st), device, _stream_handle(stream), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.device = device
+        self.n_obj = int(lib.podp_n_obj(h))
+        self.r = int(lib.podp_r(h))
+        self.m = m
+        return self
 
     def __init__(self, ops, device: int = 0, stream=None):
         lib = load_library()

@@ -139,6 +139,37 @@ def make_illconditioned(r: int, kappa: float = 1e8, seed: int = 0) -> Operators:
     return Operators(**{**base.__dict__, "K": K})
 
 
+def make_perdir_blocks(m=(16, 16, 16), seed: int = 0, nu: float = NU_DEFAULT, alpha: float = ALPHA_DEFAULT,
+                       alpha_lb: float = 1.0) -> dict:
+    """Per-direction operator blocks for the literal N1 path (timing / GPU tests), drawn like make_operators on
+    the concatenated space n = M_1 + M_2 + M_3 and cut into blocks: K = B B^H + n I, M = C C^H (rank n/2),
+    Kb[i][j] / Cb[i][j] its M_i x M_j blocks; b0[i], b1[i] ~ CN(0,1); Hb[i][j] ~ CN(0,1) rows; S symmetric N(0,1);
+    Gx[i][j] the blocks of W^H W (W ~ CN(0,1)) on direction i's slots [b0_i, b1_i | KU_i | MU_i] (a consistent
+    PSD Gram).  Draws only -- no on-line arithmetic."""
+    rng = np.random.default_rng(seed)
+    m = [int(x) for x in m]
+    n = sum(m)
+    off = np.concatenate([[0], np.cumsum(m)])
+    B = cn(rng, (n, n), 1.0 / n)
+    K = _herm(B @ B.conj().T + n * np.eye(n))
+    C = cn(rng, (n, max(1, n // 2)), 1.0 / n)
+    M = _herm(C @ C.conj().T)
+    b0 = [cn(rng, (m[i],), 1.0) for i in range(3)]
+    b1 = [cn(rng, (m[i],), 1.0) for i in range(3)]
+    Hb = [[cn(rng, (m[j],), 1.0) for j in range(3)] for _i in range(3)]
+    S = rng.standard_normal((3, 3))
+    S = np.triu(S) + np.triu(S, 1).T
+    W = cn(rng, (2 * (6 + 2 * n), 6 + 2 * n), 1.0)
+    Gf = _herm(W.conj().T @ W)
+    slots = [np.concatenate([[2 * i, 2 * i + 1], 6 + np.arange(off[i], off[i + 1]),
+                             6 + n + np.arange(off[i], off[i + 1])]) for i in range(3)]
+    blk = lambda X, i, j: X[off[i]:off[i + 1], off[j]:off[j + 1]]  # noqa: E731
+    return dict(m=m, Kb=[[blk(K, i, j) for j in range(3)] for i in range(3)],
+                Cb=[[blk(M, i, j) for j in range(3)] for i in range(3)], b0=b0, b1=b1, Hb=Hb, N0=np.eye(3), S=S,
+                Gx=[[Gf[np.ix_(slots[i], slots[j])] for j in range(3)] for i in range(3)], nu=nu, alpha=alpha,
+                alpha_lb=alpha_lb)
+
+
 def batch_sigma(n_obj: int = 256) -> np.ndarray:
     """Config 3 conductivities: log-uniform in [1e6, 6e7] S/m from a separate stream (SURVEY 8(d) proposal)."""
     return 10.0 ** np.random.default_rng(0).uniform(6.0, math.log10(6e7), n_obj)
