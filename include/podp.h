@@ -64,9 +64,9 @@ enum {
                                    (PODP_ERR_UNSUPPORTED otherwise).  R, I, Delta are then formed as usual.
                                    The precompute runs once, on the first evaluation that asks for it.        */
   /* Solver selection, for A/B measurement (at most one; none = the measured default: PODP_FLAG_LU_LL for padded
-     r <= 64, PODP_FLAG_LU_BLK / _DYN up to 96, PODP_FLAG_LU_GENERIC above).  Every choice computes the same
+     r <= 96, PODP_FLAG_LU_GENERIC above).  Every choice computes the same
      pivoted LU solve of P:593-596 up to rounding; a choice not instantiated for this r -> PODP_ERR_UNSUPPORTED. */
-  PODP_FLAG_LU_LL = 1u << 8,      /* left-looking block LU, one warp per frequency, padded r <= 64 (k_lu_ll.cu) */
+  PODP_FLAG_LU_LL = 1u << 8,      /* left-looking block LU, one warp per frequency, padded r <= 96 (k_lu_ll.cu) */
   PODP_FLAG_LU_BLK = 1u << 9,     /* lock-step panel-blocked LU, W warps per frequency, padded r <= 96        */
   PODP_FLAG_LU_DYN = 1u << 10,    /* dynamically scheduled blocked LU, W warps per frequency, padded r <= 96  */
   PODP_FLAG_LU_GENERIC = 1u << 11 /* generic one-warp LU (any r <= 128, pivoting or PODP_FLAG_NO_PIVOT)       */

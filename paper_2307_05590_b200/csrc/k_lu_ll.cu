@@ -1,4 +1,4 @@
-// K2 default path (R <= 64): left-looking block LU with partial pivoting + 3-RHS solve, ONE WARP PER FREQUENCY
+// K2 default path (R <= 96): left-looking block LU with partial pivoting + 3-RHS solve, ONE WARP PER FREQUENCY
 // (rows a2-a3 of SURVEY 8(a)).
 //   A(omega) = K + i omega nu M,  B(omega) = b0 + omega b1,  P = A^{-1} B            (eqn:ReducedA)
 //
@@ -21,6 +21,9 @@
 //   and M rows at assembly time and the M strips of earlier panels are re-ordered only when a panel interchanged
 //   rows.  The 3-column right-hand side is real-ified (8 x [Re | Im] columns): a complex 8x8 by 8x3 product is 4 DMMA.
 //   One warp owns one frequency end to end (no inter-warp synchronisation); G independent warps per CTA.
+//   Shared memory per warp holds only the M tiles (NT(NT-1)/2) plus one tile for the current panel's diagonal block
+//   (see strip_off): the diagonal blocks go to the L2 scratch with the Y tiles, which buys warps per SM (r = 48:
+//   12 instead of 10, r = 96: 3 instead of 2; measured 3.47 -> 3.29 ms and 48.4 -> 33.1 ms per 1e5 frequencies).
 #include <utility>
 
 #include "podp_common.cuh"
@@ -38,24 +41,41 @@ namespace lull {
 
 template <int R>
 struct Cfg {
-  static_assert(R % 8 == 0 && R >= 8 && R <= 64, "left-looking kernel: R in 8..64, multiple of 8");
+  static_assert(R % 8 == 0 && R >= 8 && R <= 96, "left-looking kernel: R in 8..96, multiple of 8");
   static constexpr int NT = R / 8;                       // tile rows / columns
-  static constexpr int STRIP_TILES = NT * (NT + 1) / 2;  // strip b holds tiles b..NT-1 (diag tile = L\U)
+  // DIAG_L2 (R >= 40, where shared memory bounds the warps per SM): shared memory per warp holds the M tiles of
+  // every strip (strip b: tiles b+1..NT-1) plus one tile for the diagonal block of the panel being factored (see
+  // strip_off), and the diagonal blocks go to the L2 scratch; below, strip b holds tiles b..NT-1 including its
+  // diagonal block (measured faster there: no copy-out, and the warp count is capped by registers anyway)
+  static constexpr bool DIAG_L2 = R >= 40;
+  static constexpr int STRIP_TILES = DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2;
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
   static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16;
   static constexpr int G_SMEM = (227 * 1024) / W_BYTES;
+  // warp cap (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition, 224-255
+  // above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
+  static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);
 #ifdef PODP_LL_G  // dev: fewer warps per CTA (occupancy experiments)
-  static constexpr int G = G_SMEM < PODP_LL_G ? G_SMEM : PODP_LL_G;
+  static constexpr int G_MAX = PODP_LL_G;
 #else
-  static constexpr int G = G_SMEM < 16 ? G_SMEM : 16;    // warps (= concurrent frequencies) per CTA
+  static constexpr int G_MAX = G_REG;
 #endif
-  static constexpr int GSCR_TILES = NT * (NT + 1) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT
+  static constexpr int G = G_SMEM < G_MAX ? G_SMEM : G_MAX;  // warps (= concurrent frequencies) per CTA
+  static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
   static constexpr size_t BYTES = (size_t)G * W_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
 };
 
-// first tile of strip b
-__host__ __device__ constexpr int strip_off(int NT, int b) { return b * NT - b * (b - 1) / 2; }
+// Shared-memory tile offset of the "virtual strip" of panel b: its diagonal-block tile followed by its M tiles
+// (tiles b+1..NT-1).  Without DIAG_L2 the strips are simply consecutive (strip b = tiles b..NT-1).  With DIAG_L2 the
+// strips are stored in reverse order after one spare tile, [spare | strip NT-2 | strip NT-3 | ... | strip 0] (M tiles
+// only), so the diagonal-block tile of panel b is the last tile of strip b+1 (or the spare tile): space that is
+// written only after panel b has copied its diagonal block to the L2 scratch.  Every access to the M tiles of strip
+// b is at tile offset >= 1 from strip_off(b), in both layouts.
+template <bool DIAG_L2>
+__host__ __device__ constexpr int strip_off(int NT, int b) {
+  return DIAG_L2 ? (NT - 2 - b) * (NT - 1 - b) / 2 : b * NT - b * (b - 1) / 2;
+}
 // row swizzle: slot = k ^ swz(i & 7) makes both lane = row reads (8 rows, same k) and A-fragment reads (rows 2j,
 // 2j+1 x 4 consecutive k) hit 8 distinct 16-byte bank groups
 __device__ __forceinline__ int swz(int i) { return ((i & 1) << 2) | ((i >> 1) & 3); }
@@ -105,7 +125,7 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], c
     nyi[s] = -i;
   }
   const int r4 = lane >> 2, q = lane & 3;
-  const double2 *Sb = S + strip_off(NT, B) * 64;
+  const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
@@ -143,7 +163,7 @@ __device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, i
     b2[s] = -b2[s];
   }
   const int r4 = lane >> 2, q = lane & 3;
-  const double2 *Sb = S + strip_off(NT, B) * 64;
+  const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
@@ -167,10 +187,10 @@ __device__ __forceinline__ double2 afrag_cstore(const double2 *g, int s, int lan
 // interchanges applied to perm and to the strips of earlier panels.  Returns 0 or (LAPACK getrf info) k + 1 for
 // an exactly zero pivot column at global step k.
 template <int R, int MSE, bool PIVOT>
-__device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, int lane) {
+__device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, double2 *gDiag, int lane) {
   constexpr int NT = R / 8;
   const int kb = 8 * c;
-  double2 *St = S + strip_off(NT, c) * 64;
+  double2 *St = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, c) * 64;
   double2 pn[MSE][8], urc[MSE];
   int pos[MSE], q0[MSE], pv[MSE];
 #pragma unroll
@@ -267,7 +287,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     for (int m = 0; m < MSE; ++m)
       if (pos[m] < R && pos[m] != q0[m]) sPerm[pos[m]] = pv[m];
     for (int b = 0; b < c; ++b) {
-      double2 *Sb = S + strip_off(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
+      double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
 #pragma unroll
       for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
         double2 tmp[MSE][4];
@@ -289,6 +309,13 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     }
   }
   __syncwarp();
+  if constexpr (Cfg<R>::DIAG_L2) {
+    // the diagonal block (L_cc \ U_cc with 1/U_kk on the diagonal, swizzled rows) -> L2 scratch for the inverses;
+    // its shared-memory tile is reused by the next strip
+    gDiag[c * 64 + 2 * lane] = St[2 * lane];
+    gDiag[c * 64 + 2 * lane + 1] = St[2 * lane + 1];
+    __syncwarp();
+  }
   return 0;
 }
 
@@ -308,6 +335,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
   const int64_t gw = (int64_t)blockIdx.x * G + wid, nw = (int64_t)gridDim.x * G;
   double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
   double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
+  double2 *gDiag = gD + NT * 64;  // L\U diagonal blocks (panel order)
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
 
   // (obj, f) of evaluation t, advanced incrementally (no 64-bit division, whose subroutine call forces spills)
@@ -346,7 +374,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
           for (int b = 0; b < c; ++b) lull::body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
         // ---- panel c: tiles c..NT-1 -> strip c, then unblocked LU with pivoting --------------------------------
         {
-          double2 *St = S + lull::strip_off(NT, c) * 64;
+          double2 *St = S + lull::strip_off<C::DIAG_L2>(NT, c) * 64;
 #pragma unroll
           for (int tt = 0; tt < NT; ++tt) {
             if (tt >= c) {
@@ -360,10 +388,10 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
         if constexpr (PODP_LL_ABLATE & 1) {
           info = 0;
         } else if constexpr (C::MS > 1) {
-          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT>(c, S, sRow, sPerm, lane)
-                                  : lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, lane);
+          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT>(c, S, sRow, sPerm, gDiag, lane)
+                                  : lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, gDiag, lane);
         } else {
-          info = lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, lane);
+          info = lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, gDiag, lane);
         }
         if (info != 0) break;
       }
@@ -400,7 +428,8 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
           for (int t0 = 0; t0 < NT; t0 += 4) {
             const int td = t0 + (lane >> 3);
             if (td < NT) {
-              const double2 *Dg = S + lull::strip_off(NT, td) * 64;  // rows 0..7 of strip td: L\U diagonal block
+              // L\U diagonal block of panel td: L2 scratch (written by this warp) or rows 0..7 of strip td
+              const double2 *Dg = C::DIAG_L2 ? gDiag + td * 64 : S + lull::strip_off<false>(NT, td) * 64;
               double2 y[8], x[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -499,17 +528,18 @@ static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
 }  // namespace lull
 
 size_t lu_ll_scratch_bytes(int R, int sms) {
-  if (R % 8 || R > 64) return 0;
+  if (R % 8 || R > 96) return 0;
   const int NT = R / 8;
   int G = 0;
   switch (R) {
 #define PODP_CASE(RR) \
   case RR: G = lull::Cfg<RR>::G; break;
     PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+    PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
 #undef PODP_CASE
     default: return 0;
   }
-  return (size_t)sms * G * (NT * (NT + 1) / 2) * 1024;
+  return (size_t)sms * G * (NT * (NT + 3) / 2) * 1024;
 }
 
 cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
@@ -523,6 +553,10 @@ cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
     case 48: return lull::launch_t<48>(a, s, sms);
     case 56: return lull::launch_t<56>(a, s, sms);
     case 64: return lull::launch_t<64>(a, s, sms);
+    case 72: return lull::launch_t<72>(a, s, sms);
+    case 80: return lull::launch_t<80>(a, s, sms);
+    case 88: return lull::launch_t<88>(a, s, sms);
+    case 96: return lull::launch_t<96>(a, s, sms);
     default: return cudaErrorNotSupported;
   }
 }

@@ -515,12 +515,12 @@ namespace {
 
 enum SolverKind { K_LL, K_BLK, K_DYN, K_GEN, K_PENCIL };
 
-// Solver for padded size R: the one-warp left-looking kernel for R <= 64, the blocked multi-warp kernels (measured
-// table) up to 96, the generic kernel beyond (and for NO_PIVOT above 64); PODP_FLAG_LU_* overrides (A/B).
+// Solver for padded size R: the one-warp left-looking kernel up to R = 96 (pivoting or PODP_FLAG_NO_PIVOT), the
+// generic kernel beyond; PODP_FLAG_LU_* overrides (A/B: the lock-step and dynamically scheduled blocked kernels).
 podp_status pick_solver(int R, int flags, SolverKind *ker) {
   const int lu_sel = flags & (PODP_FLAG_LU_LL | PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC);
   if (lu_sel & (lu_sel - 1)) return fail(PODP_ERR_ARG, "at most one PODP_FLAG_LU_* solver may be requested");
-  if ((lu_sel == PODP_FLAG_LU_LL && R > 64) || ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && R > 96))
+  if ((lu_sel == PODP_FLAG_LU_LL && R > 96) || ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && R > 96))
     return fail(PODP_ERR_UNSUPPORTED, "requested LU kernel is not instantiated for padded r = %d", R);
   if ((lu_sel == PODP_FLAG_LU_BLK || lu_sel == PODP_FLAG_LU_DYN) && (flags & PODP_FLAG_NO_PIVOT))
     return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_LU_BLK / _DYN always pivot");
@@ -529,9 +529,7 @@ podp_status pick_solver(int R, int flags, SolverKind *ker) {
   else if (lu_sel == PODP_FLAG_LU_BLK) *ker = K_BLK;
   else if (lu_sel == PODP_FLAG_LU_DYN) *ker = K_DYN;
   else if (lu_sel == PODP_FLAG_LU_GENERIC) *ker = K_GEN;
-  else if (R <= 64) *ker = K_LL;
-  else if (flags & PODP_FLAG_NO_PIVOT) *ker = K_GEN;
-  else if (R <= 96) *ker = (R == 72 || R >= 80) ? K_DYN : K_BLK;
+  else if (R <= 96) *ker = K_LL;  // measured fastest at every padded R = 8 .. 96 (profiles/r02_luab_layout.txt)
   else *ker = K_GEN;
   return PODP_OK;
 }

@@ -111,7 +111,7 @@ def test_no_pivot_flag_parity(torch_cuda, r):
 def _lu_flags(r):
     from paper_2307_05590_b200 import FLAG_LU_LL, FLAG_LU_BLK, FLAG_LU_DYN, FLAG_LU_GENERIC
     out = [("blk", FLAG_LU_BLK), ("dyn", FLAG_LU_DYN), ("generic", FLAG_LU_GENERIC)]
-    if r <= 64:
+    if r <= 96:
         out.insert(0, ("ll", FLAG_LU_LL))
     return out
 
@@ -211,10 +211,10 @@ def test_all_lu_kernels_parity_and_singular(torch_cuda, r):
 def test_lu_kernel_selection_errors(torch_cuda):
     from paper_2307_05590_b200 import Evaluator, PodpError, FLAG_LU_LL, FLAG_LU_BLK, FLAG_NO_PIVOT
     torch = torch_cuda
-    ev = Evaluator(g.make_operators(96))
+    ev = Evaluator(g.make_operators(104))
     w = torch.tensor(g.omega_grid(5), device="cuda")
     with pytest.raises(PodpError) as ei:
-        ev.eval(w, flags=FLAG_LU_LL)            # not instantiated above padded r = 64
+        ev.eval(w, flags=FLAG_LU_LL)            # not instantiated above padded r = 96
     assert ei.value.status == 4
     with pytest.raises(PodpError) as ei:
         ev.eval(w, flags=FLAG_LU_LL | FLAG_LU_BLK)

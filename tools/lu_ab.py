@@ -26,7 +26,7 @@ def main():
         ev = Evaluator(g.make_operators(r))
         out = ev.alloc_outputs(F)
         R = (r + 7) // 8 * 8
-        variants = [("ll", FLAG_LU_LL)] if R <= 64 else []
+        variants = [("ll", FLAG_LU_LL)] if R <= 96 else []
         if R <= 96:
             variants += [("blk", FLAG_LU_BLK), ("dyn", FLAG_LU_DYN)]
         if os.environ.get("LU_AB_GENERIC"):
