@@ -502,7 +502,7 @@ def main():
         dom_flops = F * (falg_solve(R_HEAD) if dom == "solve" else falg_mpt(R_HEAD))
         achieved = dom_flops / (dom_ms / 1e3) / 1e12
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+        tpath = os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")
         if os.path.exists(tpath):
             try:
                 traffic = json.load(open(tpath)).get(dom, {}).get("dram_bytes_per_launch")

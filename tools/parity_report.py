@@ -57,6 +57,7 @@ def main():
         pl = np.zeros(3)
         normw = np.zeros(3)
         above, adjudicated_ok = 0, 0
+        details = []
         for o, f in pairs:
             ops = ops_list[o]
             w = float(omega[f])
@@ -78,14 +79,22 @@ def main():
                         floor = 1e-3 * np.max(np.abs(t6))
                         eg = abs(g6[q][b] - t6[b])
                         eo = abs(o6[q][b] - t6[b])
-                        if eg <= 2.0 * eo or eg <= 1e-10 * max(abs(t6[b]), floor):
-                            adjudicated_ok += 1
+                        ok = eg <= 2.0 * eo or eg <= 1e-10 * max(abs(t6[b]), floor)
+                        adjudicated_ok += int(ok)
+                        from oracle.parity import magnitudes
+                        mg = magnitudes(ops, w)[q][b]
+                        if len(details) < 8:
+                            details.append({"obj": int(o), "omega": w, "quantity": "RID"[q], "entry": int(b),
+                                            "value_80bit": float(t6[b]), "gpu_err": float(eg),
+                                            "fp64_oracle_err": float(eo), "term_magnitude": float(mg),
+                                            "gpu_err_over_magnitude": float(eg / mg) if mg > 0 else None,
+                                            "within_2x_oracle": bool(ok)})
         rec = {"config": c["spec"]["name"], "r": c["spec"]["r"], "evaluations": F * len(ops_list),
                "sampled": len(pairs), "gate_max_normalised": dict(zip(("R", "I", "Delta"), gate.tolist())),
                "gate_pass": bool(np.all(gate <= 1.0)),
                "plain_rel_1e-3_floor_max": dict(zip(("R", "I", "Delta"), pl.tolist())),
                "normwise_max": dict(zip(("R", "I", "Delta"), normw.tolist())),
-               "plain_above_1e-10": above, "adjudicated_80bit_ok": adjudicated_ok,
+               "plain_above_1e-10": above, "adjudicated_80bit_ok": adjudicated_ok, "above_details": details,
                "seconds": round(time.time() - t0, 1)}
         print(json.dumps(rec), flush=True)
 
