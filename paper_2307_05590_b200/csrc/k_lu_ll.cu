@@ -321,13 +321,168 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
 
 }  // namespace lull
 
+namespace lull {
+
+// a2 + the left-looking updates of column tile c for one frequency: A[perm rows, c] = K + i s M gathered into C
+// fragments, minus sum_{b < c} M_{:,b} Y_{b,c} (DMMA), then rows >= 8c to the panel's virtual strip.
+template <int R>
+__device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], double (&ai)[R / 8][2], double2 *S,
+                                            double2 *gY, const int *sPerm, const double2 *gK, const double2 *gM,
+                                            double s, int lane) {
+  using C = Cfg<R>;
+  constexpr int NT = C::NT;
+  const int r4 = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int tt = 0; tt < NT; ++tt) {
+    const int ph = sPerm[8 * tt + r4];
+    const double2 *kp = gK + (size_t)ph * R + 8 * c + 2 * q, *mp = gM + (size_t)ph * R + 8 * c + 2 * q;
+    const double2 k0 = __ldg(kp), k1 = __ldg(kp + 1), m0 = __ldg(mp), m1 = __ldg(mp + 1);
+    ar[tt][0] = fma(-s, m0.y, k0.x);
+    ai[tt][0] = fma(s, m0.x, k0.y);
+    ar[tt][1] = fma(-s, m1.y, k1.x);
+    ai[tt][1] = fma(s, m1.x, k1.y);
+  }
+  if constexpr (!(PODP_LL_ABLATE & 2))
+    for (int b = 0; b < c; ++b) body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
+  double2 *St = S + strip_off<C::DIAG_L2>(NT, c) * 64;
+#pragma unroll
+  for (int tt = 0; tt < NT; ++tt) {
+    if (tt >= c) {
+      double2 *row = St + (8 * (tt - c) + r4) * 8;
+      row[(2 * q) ^ swz(r4)] = make_double2(ar[tt][0], ai[tt][0]);
+      row[(2 * q + 1) ^ swz(r4)] = make_double2(ar[tt][1], ai[tt][1]);
+    }
+  }
+}
+
+// After the factorisation of one frequency: z = P_perm B (real-ified: cols [Re b_0..2 | Im b_0..2 | 0 0]), forward
+// sweep, diagonal-block inverses D_t, block back substitution, P written (workspace and optional debug output).
+template <int R>
+__device__ __forceinline__ void finish(const EvalArgs &a, const double *op, double om, const double2 *S,
+                                       double2 *gY, double2 *gD, const double2 *gDiag, const int *sPerm, double *Pw,
+                                       int64_t t, int lane) {
+  using C = Cfg<R>;
+  constexpr int NT = C::NT;
+  const int r4 = lane >> 2, q = lane & 3;
+  double z[NT][2];
+  {
+    const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
+    const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+      const int ph = sPerm[8 * tt + r4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * q + e;
+        double v = 0.0;
+        if (n < 6) {
+          const int d = n < 3 ? n : n - 3;
+          const double2 x0 = __ldg(gb0 + d * R + ph), x1 = __ldg(gb1 + d * R + ph);
+          v = n < 3 ? fma(om, x1.x, x0.x) : fma(om, x1.y, x0.y);
+        }
+        z[tt][e] = v;
+      }
+    }
+  }
+  if constexpr (!(PODP_LL_ABLATE & 8))
+    [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
+      (body_rhs<NT, Bs>(z, S, lane), ...);
+    }(std::make_integer_sequence<int, NT - 1>{});
+  // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----------
+  if constexpr (!(PODP_LL_ABLATE & 4)) {
+    const int j = lane & 7;
+#pragma unroll 1
+    for (int t0 = 0; t0 < NT; t0 += 4) {
+      const int td = t0 + (lane >> 3);
+      if (td < NT) {
+        // L\U diagonal block of panel td: L2 scratch (written by this warp) or rows 0..7 of strip td
+        const double2 *Dg = C::DIAG_L2 ? gDiag + td * 64 : S + strip_off<false>(NT, td) * 64;
+        double2 y[8], x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          double2 acc = make_double2(i == j ? 1.0 : 0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < i; ++k) acc = cfms(Dg[i * 8 + (k ^ swz(i))], y[k], acc);
+          y[i] = acc;
+        }
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          double2 acc = y[i];
+#pragma unroll
+          for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ swz(i))], x[k], acc);
+          x[i] = cmul(acc, Dg[i * 8 + (i ^ swz(i))]);  // 1/U_ii (stored by the panel)
+        }
+        double2 *dt = gD + td * 64;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+      }
+    }
+  }
+  __syncwarp();
+  // ---- block back substitution x_t = D_t (z_t - sum_{c > t} Y_tc x_c), right-looking over c -----------------
+#pragma unroll
+  for (int tt = NT - 1; tt >= 0; --tt) {
+    double b1[2], b2[2];
+    rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
+    const double2 d0 = afrag_cstore(gD + tt * 64, 0, lane), d1 = afrag_cstore(gD + tt * 64, 1, lane);
+    double x0 = 0.0, x1 = 0.0;
+    dmma(x0, x1, d0.x, b1[0]);
+    dmma(x0, x1, d0.y, b2[0]);
+    dmma(x0, x1, d1.x, b1[1]);
+    dmma(x0, x1, d1.y, b2[1]);
+    // P (3 x R complex, direction-major): column n of the real-ified tile = Re (n < 3) / Im (3 <= n < 6)
+    {
+      const int i = 8 * tt + r4;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * q + e;
+        if (n < 6) {
+          const int d = n < 3 ? n : n - 3, part = n < 3 ? 0 : 1;
+          const double v = e ? x1 : x0;
+          Pw[(d * R + i) * 2 + part] = v;
+          if (a.P_out && i < a.r) a.P_out[(((size_t)t * 3 + d) * a.r + i) * 2 + part] = v;
+        }
+      }
+    }
+    if (tt > 0 && !(PODP_LL_ABLATE & 8)) {
+      rhs_frags(x0, x1, lane, b1, b2);
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        b1[s2] = -b1[s2];
+        b2[s2] = -b2[s2];
+      }
+#pragma unroll
+      for (int t2 = 0; t2 < tt; ++t2) {
+        const double2 *gyt = gY + (tt * (tt - 1) / 2 + t2) * 64;
+        const double2 y0 = afrag_cstore(gyt, 0, lane), y1 = afrag_cstore(gyt, 1, lane);
+        dmma(z[t2][0], z[t2][1], y0.x, b1[0]);
+        dmma(z[t2][0], z[t2][1], y0.y, b2[0]);
+        dmma(z[t2][0], z[t2][1], y1.x, b1[1]);
+        dmma(z[t2][0], z[t2][1], y1.y, b2[1]);
+      }
+    }
+  }
+}
+
+// info != 0: the frequency's P is NaN (and its info code is written)
+__device__ __forceinline__ void fail_out(const EvalArgs &a, double *Pw, int R, int64_t t, int info, int lane) {
+  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
+  if (info != 0) {
+    for (int e = lane; e < 6 * R; e += 32) Pw[e] = nanv;
+    if (a.P_out)
+      for (int e = lane; e < 6 * a.r; e += 32) a.P_out[(size_t)t * 6 * a.r + e] = nanv;
+  }
+  if (a.info && lane == 0) a.info[t] = info;
+}
+
+}  // namespace lull
+
 template <int R, bool PIVOT>
 __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
   using C = lull::Cfg<R>;
   constexpr int NT = C::NT, G = C::G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r4 = lane >> 2, q = lane & 3;
   double2 *S = reinterpret_cast<double2 *>(smem_raw + (size_t)wid * C::W_BYTES);
   double2 *sRow = S + C::STRIP_TILES * 64;
   int *sPerm = reinterpret_cast<int *>(sRow + 9);
@@ -336,7 +491,6 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
   double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
   double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
   double2 *gDiag = gD + NT * 64;  // L\U diagonal blocks (panel order)
-  const double nanv = __longlong_as_double(0x7ff8000000000000ll);
 
   // (obj, f) of evaluation t, advanced incrementally (no 64-bit division, whose subroutine call forces spills)
   int obj = 0;
@@ -358,32 +512,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
       __syncwarp();
       double ar[NT][2], ai[NT][2];
       for (int c = 0; c < NT; ++c) {
-        // ---- a2: column tile c of A = K + i s M, rows gathered through perm (C fragments) --------------------
-#pragma unroll
-        for (int tt = 0; tt < NT; ++tt) {
-          const int ph = sPerm[8 * tt + r4];
-          const double2 *kp = gK + (size_t)ph * R + 8 * c + 2 * q, *mp = gM + (size_t)ph * R + 8 * c + 2 * q;
-          const double2 k0 = __ldg(kp), k1 = __ldg(kp + 1), m0 = __ldg(mp), m1 = __ldg(mp + 1);
-          ar[tt][0] = fma(-s, m0.y, k0.x);
-          ai[tt][0] = fma(s, m0.x, k0.y);
-          ar[tt][1] = fma(-s, m1.y, k1.x);
-          ai[tt][1] = fma(s, m1.x, k1.y);
-        }
-        // ---- a3: left-looking block updates from panels 0..c-1 (DMMA, accumulators stay in registers) ---------
-        if constexpr (!(PODP_LL_ABLATE & 2))
-          for (int b = 0; b < c; ++b) lull::body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
-        // ---- panel c: tiles c..NT-1 -> strip c, then unblocked LU with pivoting --------------------------------
-        {
-          double2 *St = S + lull::strip_off<C::DIAG_L2>(NT, c) * 64;
-#pragma unroll
-          for (int tt = 0; tt < NT; ++tt) {
-            if (tt >= c) {
-              double2 *row = St + (8 * (tt - c) + r4) * 8;
-              row[(2 * q) ^ lull::swz(r4)] = make_double2(ar[tt][0], ai[tt][0]);
-              row[(2 * q + 1) ^ lull::swz(r4)] = make_double2(ar[tt][1], ai[tt][1]);
-            }
-          }
-        }
+        lull::column_tile<R>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane);
         __syncwarp();
         if constexpr (PODP_LL_ABLATE & 1) {
           info = 0;
@@ -395,114 +524,9 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
         }
         if (info != 0) break;
       }
-      if (info == 0) {
-        // ---- right-hand side z = P_perm B (real-ified: cols [Re b_0..2 | Im b_0..2 | 0 0]) and forward sweep ----
-        double z[NT][2];
-        {
-          const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
-          const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
-#pragma unroll
-          for (int tt = 0; tt < NT; ++tt) {
-            const int ph = sPerm[8 * tt + r4];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int n = 2 * q + e;
-              double v = 0.0;
-              if (n < 6) {
-                const int d = n < 3 ? n : n - 3;
-                const double2 x0 = __ldg(gb0 + d * R + ph), x1 = __ldg(gb1 + d * R + ph);
-                v = n < 3 ? fma(om, x1.x, x0.x) : fma(om, x1.y, x0.y);
-              }
-              z[tt][e] = v;
-            }
-          }
-        }
-        if constexpr (!(PODP_LL_ABLATE & 8))
-          [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
-            (lull::body_rhs<NT, Bs>(z, S, lane), ...);
-          }(std::make_integer_sequence<int, NT - 1>{});
-        // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----
-        if constexpr (!(PODP_LL_ABLATE & 4)) {
-          const int j = lane & 7;
-#pragma unroll 1
-          for (int t0 = 0; t0 < NT; t0 += 4) {
-            const int td = t0 + (lane >> 3);
-            if (td < NT) {
-              // L\U diagonal block of panel td: L2 scratch (written by this warp) or rows 0..7 of strip td
-              const double2 *Dg = C::DIAG_L2 ? gDiag + td * 64 : S + lull::strip_off<false>(NT, td) * 64;
-              double2 y[8], x[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                double2 acc = make_double2(i == j ? 1.0 : 0.0, 0.0);
-#pragma unroll
-                for (int k = 0; k < i; ++k) acc = cfms(Dg[i * 8 + (k ^ lull::swz(i))], y[k], acc);
-                y[i] = acc;
-              }
-#pragma unroll
-              for (int i = 7; i >= 0; --i) {
-                double2 acc = y[i];
-#pragma unroll
-                for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ lull::swz(i))], x[k], acc);
-                x[i] = cmul(acc, Dg[i * 8 + (i ^ lull::swz(i))]);  // 1/U_ii (stored by the panel)
-              }
-              double2 *dt = gD + td * 64;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
-            }
-          }
-        }
-        __syncwarp();
-        // ---- block back substitution x_t = D_t (z_t - sum_{c > t} Y_tc x_c), right-looking over c -------------
-#pragma unroll
-        for (int tt = NT - 1; tt >= 0; --tt) {
-          double b1[2], b2[2];
-          lull::rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
-          const double2 d0 = lull::afrag_cstore(gD + tt * 64, 0, lane), d1 = lull::afrag_cstore(gD + tt * 64, 1, lane);
-          double x0 = 0.0, x1 = 0.0;
-          lull::dmma(x0, x1, d0.x, b1[0]);
-          lull::dmma(x0, x1, d0.y, b2[0]);
-          lull::dmma(x0, x1, d1.x, b1[1]);
-          lull::dmma(x0, x1, d1.y, b2[1]);
-          // P (3 x R complex, direction-major): column n of the real-ified tile = Re (n < 3) / Im (3 <= n < 6)
-          {
-            const int i = 8 * tt + r4;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int n = 2 * q + e;
-              if (n < 6) {
-                const int d = n < 3 ? n : n - 3, part = n < 3 ? 0 : 1;
-                const double v = e ? x1 : x0;
-                Pw[(d * R + i) * 2 + part] = v;
-                if (a.P_out && i < a.r) a.P_out[(((size_t)t * 3 + d) * a.r + i) * 2 + part] = v;
-              }
-            }
-          }
-          if (tt > 0 && !(PODP_LL_ABLATE & 8)) {
-            lull::rhs_frags(x0, x1, lane, b1, b2);
-#pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-              b1[s2] = -b1[s2];
-              b2[s2] = -b2[s2];
-            }
-#pragma unroll
-            for (int t2 = 0; t2 < tt; ++t2) {
-              const double2 *gyt = gY + (tt * (tt - 1) / 2 + t2) * 64;
-              const double2 y0 = lull::afrag_cstore(gyt, 0, lane), y1 = lull::afrag_cstore(gyt, 1, lane);
-              lull::dmma(z[t2][0], z[t2][1], y0.x, b1[0]);
-              lull::dmma(z[t2][0], z[t2][1], y0.y, b2[0]);
-              lull::dmma(z[t2][0], z[t2][1], y1.x, b1[1]);
-              lull::dmma(z[t2][0], z[t2][1], y1.y, b2[1]);
-            }
-          }
-        }
-      }
+      if (info == 0) lull::finish<R>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane);
     }
-    if (info != 0) {
-      for (int e = lane; e < 6 * R; e += 32) Pw[e] = nanv;
-      if (a.P_out)
-        for (int e = lane; e < 6 * a.r; e += 32) a.P_out[(size_t)t * 6 * a.r + e] = nanv;
-    }
-    if (a.info && lane == 0) a.info[t] = info;
+    lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
     f += nw;
     while (f >= a.F) {
