@@ -83,8 +83,17 @@ __global__ void select_arg_kernel(const double *__restrict__ omega, const double
 // result layout (doubles): [0] n_new, [1] Lambda, [2 .. 2+n_int) Lambda_n (-1 = empty),
 // then n_star grid indices, then n_star omegas (both ascending by index; unused slots -1 / NaN).
 __global__ void select_final_kernel(const double *__restrict__ omega, int n_int, int n_star, double theta,
-                                    const unsigned long long *lam_key, const unsigned long long *arg_idx,
+                                    const unsigned long long *g_lam_key, const unsigned long long *g_arg_idx,
                                     double *result) {
+  // the per-interval keys and indices are staged in shared memory by the whole block first (independent loads), so
+  // the serial choice below does not wait on one L2 round trip per read
+  extern __shared__ unsigned long long s_ka[];
+  unsigned long long *lam_key = s_ka, *arg_idx = s_ka + n_int;
+  for (int n = threadIdx.x; n < n_int; n += blockDim.x) {
+    lam_key[n] = g_lam_key[n];
+    arg_idx[n] = g_arg_idx[n];
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double lam_g = -1.0;
   int n_cand = 0;
@@ -147,7 +156,8 @@ cudaError_t launch_select(const double *omega, const double *Delta, int64_t F, c
   const size_t sm = sizeof(double) * n_snap;
   select_max_kernel<<<(unsigned)blocks, 256, sm, s>>>(omega, Delta, F, snap_d, n_snap, lam_key);
   select_arg_kernel<<<(unsigned)blocks, 256, sm, s>>>(omega, Delta, F, snap_d, n_snap, lam_key, arg_idx);
-  select_final_kernel<<<1, 32, 0, s>>>(omega, n_int, n_star, theta, lam_key, arg_idx, result_d);
+  select_final_kernel<<<1, 128, 2 * sizeof(unsigned long long) * n_int, s>>>(omega, n_int, n_star, theta, lam_key,
+                                                                             arg_idx, result_d);
   *nlaunch += 3;
   return cudaGetLastError();
 }
