@@ -199,6 +199,12 @@ int32_t podp_profile_read(char *names, double *ms, int64_t *counts, int32_t max_
 podp_status podp_destroy(podp_ctx *ctx);
 
 /* Thread-local message of the last non-OK status ("" if none). */
+/* Workspace memory (the P hand-off, LU and select scratch) comes from one stream-ordered pool per device that the
+ * library keeps for the process lifetime, so evaluations reuse mapped memory across calls and contexts.  This
+ * returns the pool's unused memory to the driver (cudaMemPoolTrimTo 0); safe at any time (in-flight evaluations keep
+ * their allocations).  PODP_OK, or PODP_ERR_ARG for a device the library has not used. */
+podp_status podp_release_workspace(int device);
+
 const char *podp_last_error(void);
 
 /* Library version string. */

@@ -235,6 +235,35 @@ void pack(const podp_operators &o, const podp::Layout &L, double *dst) {
   }
 }
 
+// One stream-ordered memory pool per device for the whole library (P hand-off workspaces, LU scratch, select
+// scratch), created on first use and kept for the process: its release threshold is infinite, so steady-state
+// evaluations -- across contexts too, e.g. the one context per iteration of the Algorithm-1 driver -- reuse mapped
+// memory instead of paying for a fresh pool and fresh mappings per context.
+std::mutex g_pool_mu;
+std::vector<cudaMemPool_t> g_pools;
+
+cudaError_t library_pool(int device, cudaMemPool_t *out) {
+  std::mutex &mu = g_pool_mu;
+  std::vector<cudaMemPool_t> &pools = g_pools;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+  if (!pools[device]) {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    cudaError_t e = cudaMemPoolCreate(&pool, &pp);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;  // never trim
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[device] = pool;
+  }
+  *out = pools[device];
+  return cudaSuccess;
+}
+
 // Padded size: next multiple of 8 (the specialised kernels exist for R = 8, 16, ..., 128); the padding is exact
 // (K_pad = diag(K, I), every other operator zero-padded).
 int choose_R(int r) { return (r + 7) / 8 * 8; }
@@ -340,6 +369,16 @@ Layout make_layout(int R) {
 extern "C" {
 
 const char *podp_last_error(void) { return g_err.c_str(); }
+
+podp_status podp_release_workspace(int device) {
+  g_err.clear();
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (device < 0 || device >= (int)g_pools.size() || !g_pools[device])
+    return fail(PODP_ERR_ARG, "no workspace pool on device %d", device);
+  cudaError_t e = cudaMemPoolTrimTo(g_pools[device], 0);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemPoolTrimTo");
+  return PODP_OK;
+}
 const char *podp_version(void) { return "podp-b200 0.1 (sm_100a, fp64)"; }
 int32_t podp_last_launch_count(void) { return g_last_launches; }
 int32_t podp_n_obj(const podp_ctx *c) { return c ? c->n_obj : 0; }
@@ -360,40 +399,30 @@ podp_status podp_create_batch(int32_t n_obj, const podp_operators *ops, int devi
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
   if (device < 0 || device >= ndev) return fail(PODP_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
-  cudaDeviceProp prop;
-  e = cudaGetDeviceProperties(&prop, device);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
-  if (prop.major != 10) return fail(PODP_ERR_UNSUPPORTED, "device %d is sm_%d%d; libpodp is built for sm_100a", device, prop.major, prop.minor);
+  int cc_major = 0, cc_minor = 0;  // (attribute queries: cudaGetDeviceProperties costs milliseconds)
+  e = cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  if (cc_major != 10) return fail(PODP_ERR_UNSUPPORTED, "device %d is sm_%d%d; libpodp is built for sm_100a", device, cc_major, cc_minor);
   DeviceGuard guard(device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", device);
   const int r = ops[0].r;
   podp::Layout L = podp::make_layout(choose_R(r));
   std::vector<double> host((size_t)L.stride * n_obj, 0.0);
   for (int k = 0; k < n_obj; ++k) pack(ops[k], L, host.data() + (size_t)L.stride * k);
+  cudaMemPool_t pool = nullptr;
+  e = library_pool(device, &pool);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemPoolCreate");
+  // the packed operators come from the library pool too (no cudaMalloc / cudaFree, which synchronise the device)
   double *d = nullptr;
-  e = cudaMalloc(&d, host.size() * sizeof(double));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(operators)");
   cudaStream_t s = (cudaStream_t)cuda_stream;
+  e = cudaMallocFromPoolAsync((void **)&d, host.size() * sizeof(double), pool, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(operators)");
   e = cudaMemcpyAsync(d, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
-    cudaFree(d);
+    cudaFreeAsync(d, s);
     return cuda_fail(e, "upload operators");
-  }
-  cudaMemPool_t pool = nullptr;
-  {
-    cudaMemPoolProps pp = {};
-    pp.allocType = cudaMemAllocationTypePinned;
-    pp.handleTypes = cudaMemHandleTypeNone;
-    pp.location.type = cudaMemLocationTypeDevice;
-    pp.location.id = device;
-    e = cudaMemPoolCreate(&pool, &pp);
-    if (e != cudaSuccess) {
-      cudaFree(d);
-      return cuda_fail(e, "cudaMemPoolCreate");
-    }
-    uint64_t thr = UINT64_MAX;  // never trim: the per-call workspace is re-used without re-mapping
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   podp_ctx *c = new podp_ctx;
   {
@@ -503,8 +532,9 @@ podp_status podp_destroy(podp_ctx *c) {
     if (c->dir[i]) podp_destroy(c->dir[i]);
   DeviceGuard guard(c->device);
   cudaDeviceSynchronize();
-  cudaFree(c->d_ops);
-  if (c->pool) cudaMemPoolDestroy(c->pool);
+  // every stream's work on the context is complete after the device synchronisation; the operators go back to the
+  // library pool (shared by every context on the device)
+  cudaFreeAsync(c->d_ops, 0);
   delete c;
   return PODP_OK;
 }

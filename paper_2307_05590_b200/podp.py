@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ER
                 5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}
 EXPORTED = ["podp_create", "podp_create_batch", "podp_create_perdir", "podp_eval", "podp_eval_host", "podp_select", "podp_n_obj", "podp_r",
             "podp_last_launch_count", "podp_destroy", "podp_last_error", "podp_version", "podp_profile_enable",
-            "podp_profile_read", "podp_invariants", "podp_coil_voltage"]
+            "podp_profile_read", "podp_invariants", "podp_coil_voltage", "podp_release_workspace"]
 
 
 class PodpError(RuntimeError):
@@ -90,8 +90,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.podp_profile_read.argtypes = [P, P, P, i32, i32]
     lib.podp_profile_read.restype = i32
     lib.podp_version.restype = ctypes.c_char_p
+    lib.podp_release_workspace.argtypes = [ctypes.c_int]
+    lib.podp_release_workspace.restype = ctypes.c_int
     _lib = lib
     return lib
+
+
+def release_workspace(device: int = 0):
+    """Return the library's unused workspace memory on `device` to the driver (podp_release_workspace)."""
+    _check(load_library().podp_release_workspace(device))
 
 
 def profile_enable(on: bool = True):

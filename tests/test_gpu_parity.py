@@ -513,3 +513,22 @@ def test_tiny_and_huge_pivots(torch_cuda, sigma):
                 eR, _eI, eD = errors(o, w, res["T1"][0, f], oracle.to6(ora["I"]), res["Delta"][0, f],
                                      oracle.to6(ora["R"]), oracle.to6(ora["I"]), oracle.to6(ora["Delta"]))
                 assert eR.max() <= TOL_RI and eD.max() <= TOL_DELTA, (r, name, w)
+
+
+def test_release_workspace_and_reuse(torch_cuda):
+    """podp_release_workspace trims the library's pool; evaluations before and after agree bit for bit."""
+    torch = torch_cuda
+    import paper_2307_05590_b200 as pb
+    ops = g.make_operators(24)
+    w = torch.tensor(g.omega_grid(3001), device="cuda")
+    ev = pb.Evaluator(ops)
+    a = ev.eval(w, flags=pb.FLAG_OUT_R)
+    torch.cuda.synchronize()
+    pb.release_workspace(0)
+    b = ev.eval(w, flags=pb.FLAG_OUT_R)
+    torch.cuda.synchronize()
+    for k in ("T1", "I", "Delta"):
+        assert torch.equal(a[k], b[k])
+    ev.close()
+    with pytest.raises(pb.PodpError):
+        pb.release_workspace(7)
