@@ -1,4 +1,6 @@
-// K3 fast path: MPT quadratic forms + error certificate, rows a4-a6 (see k_mpt.cu for the formulas / citations).
+// K3: MPT quadratic forms + error certificate, rows a4-a6 of SURVEY 8(a): R (eqn:podprealmpt), I
+// (eqn:podpimagmpt) and Delta (lemma:certificate, in the re-associated form of SURVEY
+// Appendix A.2: X_ij = c_ij + l_i p_j + conj(l_j p_i) + p_i^H Q(omega) p_j).
 //
 //   For every frequency and every pair i <= j:  Re(p_i^H K_R p_j), Re(p_i^H M p_j), Re(p_i^H Q(omega) p_j) with
 //   Q = G_KK + s J + s^2 G_MM formed on the fly (Horner, 4 DFMA per element), plus Re(l_i p_j), Re(h_i p_j).
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
       }
     }
     if (valid && sl == 0) {
-      double *T1 = a.T1 + (size_t)t * 6, *I = a.I + (size_t)t * 6, *D = a.Delta + (size_t)t * 6;
+      double T1[6], I[6], D[6];
       bool ok = isfinite(w);
 #pragma unroll
       for (int e = 0; e < 6; ++e) ok &= isfinite(qK[e]) && isfinite(qM[e]) && isfinite(qQ[e]);
@@ -255,7 +257,8 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
 #pragma unroll
         for (int e = 0; e < 6; ++e) T1[e] = I[e] = D[e] = nanv;
       } else {
-        // epilogue (same arithmetic as mpt_epilogue in k_mpt.cu)
+        // epilogue: R, I (eqn:podprealmpt / eqn:podpimagmpt) and the certificate from the
+        // reduced sums; c_ij(omega) = d^T G_{b_i b_j} d with d = (1, omega)
         const double *sc = op + a.L.scal;
         const double alpha = sc[SC_ALPHA], alb = sc[SC_ALPHA_LB];
         const double a3 = alpha * alpha * alpha;
@@ -290,6 +293,25 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
             mij = x > 0.0 ? x : 0.0;
           }
           D[e] = a3 / (8.0 * alb) * (n[i] + n[j] + mij);
+        }
+      }
+      // 48-byte output rows: three 16-byte stores per quantity when the caller's arrays are 16-byte aligned (the
+      // row offset t * 48 keeps that alignment), else six 8-byte stores
+      double *T1p = a.T1 + (size_t)t * 6, *Ip = a.I + (size_t)t * 6, *Dp = a.Delta + (size_t)t * 6;
+      if (((reinterpret_cast<uintptr_t>(a.T1) | reinterpret_cast<uintptr_t>(a.I) | reinterpret_cast<uintptr_t>(a.Delta)) &
+           15) == 0) {
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          reinterpret_cast<double2 *>(T1p)[h] = make_double2(T1[2 * h], T1[2 * h + 1]);
+          reinterpret_cast<double2 *>(Ip)[h] = make_double2(I[2 * h], I[2 * h + 1]);
+          reinterpret_cast<double2 *>(Dp)[h] = make_double2(D[2 * h], D[2 * h + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+          T1p[e] = T1[e];
+          Ip[e] = I[e];
+          Dp[e] = D[e];
         }
       }
     }

@@ -1,5 +1,6 @@
 // libpodp C ABI (include/podp.h): validation, packing (row a1 of SURVEY 8(a)), launch orchestration.
-// Host-side only; kernels live in k_solve.cu (a2-a3), k_mpt.cu (a4-a6) and k_select.cu (a7).
+// Host-side only; kernels live in k_lu_ll.cu (default a2-a3; A/B: k_lu_blk.cu, k_lu_dyn.cu, generic k_solve.cu),
+// k_mpt_tile.cu (a4-a6), k_select.cu (a7), k_pencil.cu (N3), k_perdir.cu (N1), k_epilogue.cu (N4).
 #include <cmath>
 #include <complex>
 #include <cstdarg>
@@ -753,12 +754,15 @@ podp_status podp_eval_host(const podp_ctx *c, const double *omega_h, int64_t F, 
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const size_t nout = (size_t)c->n_obj * F * 6;
-  const size_t bytes = sizeof(double) * (F + 3 * nout) + sizeof(int32_t) * (size_t)c->n_obj * F;
+  auto up = [](size_t b) { return (b + 255) / 256 * 256; };  // 256-byte aligned sub-buffers (vector stores)
+  const size_t b_om = up(sizeof(double) * F), b_out = up(sizeof(double) * nout);
+  const size_t bytes = b_om + 3 * b_out + sizeof(int32_t) * (size_t)c->n_obj * F;
   char *buf = nullptr;
   cudaError_t e = cudaMallocFromPoolAsync((void **)&buf, bytes, c->pool, s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host eval staging)");
-  double *om = (double *)buf, *T1 = om + F, *I = T1 + nout, *D = I + nout;
-  int32_t *info = (int32_t *)(D + nout);
+  double *om = (double *)buf, *T1 = (double *)(buf + b_om), *I = (double *)(buf + b_om + b_out),
+         *D = (double *)(buf + b_om + 2 * b_out);
+  int32_t *info = (int32_t *)(buf + b_om + 3 * b_out);
   e = cudaMemcpyAsync(om, omega_h, sizeof(double) * F, cudaMemcpyHostToDevice, s);
   podp_status st = PODP_OK;
   if (e == cudaSuccess) {
