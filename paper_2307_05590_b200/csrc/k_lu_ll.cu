@@ -64,6 +64,7 @@ struct Cfg {
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
   static constexpr size_t BYTES = (size_t)G * W_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
+  static_assert(!DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
 };
 
 // Shared-memory tile offset of the "virtual strip" of panel b: its diagonal-block tile followed by its M tiles
@@ -181,6 +182,11 @@ __device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, i
 __device__ __forceinline__ double2 afrag_cstore(const double2 *g, int s, int lane) {
   const int k = 4 * s + (lane & 3);
   return __ldcg(g + 2 * (4 * (lane >> 2) + (k >> 1)) + (k & 1));
+}
+// the same from shared memory
+__device__ __forceinline__ double2 afrag_cstore_s(const double2 *g, int s, int lane) {
+  const int k = 4 * s + (lane & 3);
+  return g[2 * (4 * (lane >> 2) + (k >> 1)) + (k & 1)];
 }
 
 // Unblocked LU with partial pivoting of panel c (rows 8c .. R-1 of strip c, lane = row), M_tc = L_tc L_cc^{-1},
@@ -389,14 +395,24 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
       (body_rhs<NT, Bs>(z, S, lane), ...);
     }(std::make_integer_sequence<int, NT - 1>{});
   // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----------
+  // DIAG_L2: the strips are no longer needed after the forward sweep, so the diagonal blocks are brought back from
+  // the L2 scratch into shared-memory tiles 0..NT-1 (one round of independent loads) and D_t goes to tiles
+  // NT..2NT-1, where the back substitution reads it (no L2 round trips on either chain)
+  double2 *sD = const_cast<double2 *>(S) + NT * 64;
+  if constexpr (C::DIAG_L2) {
+    __syncwarp();
+    double2 *Sw = const_cast<double2 *>(S);
+    for (int e = lane; e < NT * 64; e += 32) Sw[e] = __ldcg(gDiag + e);
+    __syncwarp();
+  }
   if constexpr (!(PODP_LL_ABLATE & 4)) {
     const int j = lane & 7;
 #pragma unroll 1
     for (int t0 = 0; t0 < NT; t0 += 4) {
       const int td = t0 + (lane >> 3);
       if (td < NT) {
-        // L\U diagonal block of panel td: L2 scratch (written by this warp) or rows 0..7 of strip td
-        const double2 *Dg = C::DIAG_L2 ? gDiag + td * 64 : S + strip_off<false>(NT, td) * 64;
+        // L\U diagonal block of panel td: staged copy (DIAG_L2) or rows 0..7 of strip td
+        const double2 *Dg = C::DIAG_L2 ? S + td * 64 : S + strip_off<false>(NT, td) * 64;
         double2 y[8], x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -412,7 +428,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
           for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ swz(i))], x[k], acc);
           x[i] = cmul(acc, Dg[i * 8 + (i ^ swz(i))]);  // 1/U_ii (stored by the panel)
         }
-        double2 *dt = gD + td * 64;
+        double2 *dt = C::DIAG_L2 ? sD + td * 64 : gD + td * 64;
 #pragma unroll
         for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
       }
@@ -424,7 +440,8 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   for (int tt = NT - 1; tt >= 0; --tt) {
     double b1[2], b2[2];
     rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
-    const double2 d0 = afrag_cstore(gD + tt * 64, 0, lane), d1 = afrag_cstore(gD + tt * 64, 1, lane);
+    const double2 d0 = C::DIAG_L2 ? afrag_cstore_s(sD + tt * 64, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
+    const double2 d1 = C::DIAG_L2 ? afrag_cstore_s(sD + tt * 64, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
     double x0 = 0.0, x1 = 0.0;
     dmma(x0, x1, d0.x, b1[0]);
     dmma(x0, x1, d0.y, b2[0]);
