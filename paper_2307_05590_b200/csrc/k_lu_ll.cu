@@ -39,7 +39,7 @@ namespace podp {
 
 namespace lull {
 
-template <int R>
+template <int R, bool KM = false>
 struct Cfg {
   static_assert(R % 8 == 0 && R >= 8 && R <= 96, "left-looking kernel: R in 8..96, multiple of 8");
   static constexpr int NT = R / 8;                       // tile rows / columns
@@ -51,7 +51,11 @@ struct Cfg {
   static constexpr int STRIP_TILES = DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2;
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
   static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16;
-  static constexpr int G_SMEM = (227 * 1024) / W_BYTES;
+  // KM (single-object launches, R <= 40): K and M staged once per CTA in shared memory (row stride R + 1 complex),
+  // so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 -> 2.10 ms per 1e5
+  // at the same 12 warps; at R >= 48 the copy would cost warps, measured slower)
+  static constexpr int KM_BYTES = KM ? 2 * R * (R + 1) * 16 : 0;
+  static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
   // warp cap (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition, 224-255
   // above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
   static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);
@@ -62,7 +66,7 @@ struct Cfg {
 #endif
   static constexpr int G = G_SMEM < G_MAX ? G_SMEM : G_MAX;  // warps (= concurrent frequencies) per CTA
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
-  static constexpr size_t BYTES = (size_t)G * W_BYTES;
+  static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
   static_assert(!DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
 };
@@ -334,15 +338,15 @@ namespace lull {
 template <int R>
 __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], double (&ai)[R / 8][2], double2 *S,
                                             double2 *gY, const int *sPerm, const double2 *gK, const double2 *gM,
-                                            double s, int lane) {
+                                            double s, int lane, int ldkm = R) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
 #pragma unroll
   for (int tt = 0; tt < NT; ++tt) {
     const int ph = sPerm[8 * tt + r4];
-    const double2 *kp = gK + (size_t)ph * R + 8 * c + 2 * q, *mp = gM + (size_t)ph * R + 8 * c + 2 * q;
-    const double2 k0 = __ldg(kp), k1 = __ldg(kp + 1), m0 = __ldg(mp), m1 = __ldg(mp + 1);
+    const double2 *kp = gK + (size_t)ph * ldkm + 8 * c + 2 * q, *mp = gM + (size_t)ph * ldkm + 8 * c + 2 * q;
+    const double2 k0 = kp[0], k1 = kp[1], m0 = mp[0], m1 = mp[1];
     ar[tt][0] = fma(-s, m0.y, k0.x);
     ai[tt][0] = fma(s, m0.x, k0.y);
     ar[tt][1] = fma(-s, m1.y, k1.x);
@@ -494,9 +498,9 @@ __device__ __forceinline__ void fail_out(const EvalArgs &a, double *Pw, int R, i
 
 }  // namespace lull
 
-template <int R, bool PIVOT>
-__global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
-  using C = lull::Cfg<R>;
+template <int R, bool PIVOT, bool KM>
+__global__ void __launch_bounds__(lull::Cfg<R, KM>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
+  using C = lull::Cfg<R, KM>;
   constexpr int NT = C::NT, G = C::G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -516,12 +520,23 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
     f -= a.F;
     ++obj;
   }
+  double2 *sKM = reinterpret_cast<double2 *>(smem_raw + (size_t)G * C::W_BYTES);
+  if constexpr (KM) {  // single-object launch: K and M of object 0 into shared memory, once per CTA
+    const double2 *k0p = reinterpret_cast<const double2 *>(a.ops + a.L.K), *m0p = reinterpret_cast<const double2 *>(a.ops + a.L.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, j = e - i * R;
+      sKM[i * (R + 1) + j] = __ldg(k0p + e);
+      sKM[R * (R + 1) + i * (R + 1) + j] = __ldg(m0p + e);
+    }
+    __syncthreads();
+  }
   for (int64_t t = gw; t < total; t += nw) {
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
-    const double2 *gK = reinterpret_cast<const double2 *>(op + a.L.K);
-    const double2 *gM = reinterpret_cast<const double2 *>(op + a.L.M);
+    const double2 *gK = C::KM_BYTES ? sKM : reinterpret_cast<const double2 *>(op + a.L.K);
+    const double2 *gM = C::KM_BYTES ? sKM + R * (R + 1) : reinterpret_cast<const double2 *>(op + a.L.M);
+    constexpr int LDKM = C::KM_BYTES ? R + 1 : R;
     double *Pw = reinterpret_cast<double *>(a.Pws + (size_t)t * 3 * R);
     int info = isfinite(om) ? 0 : -1;
     if (info == 0) {
@@ -529,7 +544,7 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
       __syncwarp();
       double ar[NT][2], ai[NT][2];
       for (int c = 0; c < NT; ++c) {
-        lull::column_tile<R>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane);
+        lull::column_tile<R>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM);
         __syncwarp();
         if constexpr (PODP_LL_ABLATE & 1) {
           info = 0;
@@ -554,10 +569,10 @@ __global__ void __launch_bounds__(lull::Cfg<R>::G * 32, 1) lu_ll_kernel(EvalArgs
 }
 
 namespace lull {
-template <int R>
-static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
-  using C = Cfg<R>;
-  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false> : lu_ll_kernel<R, true>;
+template <int R, bool KM>
+static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
+  using C = Cfg<R, KM>;
+  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false, KM> : lu_ll_kernel<R, true, KM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)a.n_obj * a.F;
@@ -565,6 +580,16 @@ static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
   if (blocks > sms) blocks = sms;
   kern<<<(unsigned)blocks, C::G * 32, C::BYTES, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
+  // K and M in shared memory only where it costs no warps (R <= 40) and the launch has one object
+  if constexpr (R <= 40) {
+    static_assert(Cfg<R, true>::G == Cfg<R, false>::G, "KM variant must keep the warp count");
+    if (a.n_obj == 1) return launch_k<R, true>(a, s, sms);
+  }
+  return launch_k<R, false>(a, s, sms);
 }
 }  // namespace lull
 
