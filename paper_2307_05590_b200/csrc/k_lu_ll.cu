@@ -39,7 +39,7 @@ namespace podp {
 
 namespace lull {
 
-template <int R, bool KM = false>
+template <int R, bool KM = false, bool TM = false>
 struct Cfg {
   static_assert(R % 8 == 0 && R >= 8 && R <= 96, "left-looking kernel: R in 8..96, multiple of 8");
   static constexpr int NT = R / 8;                       // tile rows / columns
@@ -47,28 +47,36 @@ struct Cfg {
   // every strip (strip b: tiles b+1..NT-1) plus one tile for the diagonal block of the panel being factored (see
   // strip_off), and the diagonal blocks go to the L2 scratch; below, strip b holds tiles b..NT-1 including its
   // diagonal block (measured faster there: no copy-out, and the warp count is capped by registers anyway)
-  static constexpr bool DIAG_L2 = R >= 40;
-  static constexpr int STRIP_TILES = DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2;
+  static constexpr bool DIAG_L2 = R >= 40 || TM;
+  // TM (single-object launches, 40 <= R <= 64): the M tiles live in TENSOR MEMORY (tcgen05.st / tcgen05.ld, one
+  // 8-column slice per tile in A-fragment order, this warp's 32 TMEM lanes); shared memory keeps only the current
+  // panel's virtual strip (NT tiles, also the scratch of the row interchanges and of the final inverses), so K and M
+  // fit in shared memory beside 12 warps' state (KM)
+  static constexpr int TM_TILES = NT * (NT - 1) / 2;     // M tiles per frequency (8 TMEM columns each)
+  static constexpr int STRIP_TILES = TM ? NT : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
-  static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16;
-  // KM (single-object launches, R <= 40): K and M staged once per CTA in shared memory (row stride R + 1 complex),
-  // so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 -> 2.10 ms per 1e5
-  // at the same 12 warps; at R >= 48 the copy would cost warps, measured slower)
-  static constexpr int KM_BYTES = KM ? 2 * R * (R + 1) * 16 : 0;
+  static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16 * (TM ? 2 : 1);
+  // KM (single-object launches, R <= 40, or with TM): K and M staged once per CTA in shared memory (row stride
+  // R + 1 complex), so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 ->
+  // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
+  static constexpr int KM_BYTES = (KM || TM) ? 2 * R * (R + 1) * 16 : 0;
   static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
   // warp cap (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition, 224-255
   // above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
   static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);
 #ifdef PODP_LL_G  // dev: fewer warps per CTA (occupancy experiments)
-  static constexpr int G_MAX = PODP_LL_G;
+  static constexpr int G_MAX = R <= 48 ? PODP_LL_G : G_REG;
 #else
   static constexpr int G_MAX = G_REG;
 #endif
   static constexpr int G = G_SMEM < G_MAX ? G_SMEM : G_MAX;  // warps (= concurrent frequencies) per CTA
+  // TMEM columns per warp (power-of-two stride so each of the (G + 3) / 4 warps of a sub-partition gets a slice)
+  static constexpr int TM_COLS = 8 * TM_TILES <= 64 ? 64 : (8 * TM_TILES <= 128 ? 128 : 256);
+  static_assert(!TM || TM_COLS * ((G + 3) / 4) <= 512, "M tiles do not fit in tensor memory");
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
   static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
-  static_assert(!DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
+  static_assert(TM || !DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
 };
 
 // Shared-memory tile offset of the "virtual strip" of panel b: its diagonal-block tile followed by its M tiles
@@ -90,6 +98,30 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+
+// ---- tensor memory (tcgen05) helpers: 32x32b shape, thread i <-> TMEM lane (32 * (warp % 4) + i) ---------------
+__device__ __forceinline__ void tm_st8(uint32_t taddr, double2 m0, double2 m1) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(__double2loint(m0.x)), "r"(__double2hiint(m0.x)), "r"(__double2loint(m0.y)), "r"(__double2hiint(m0.y)),
+               "r"(__double2loint(m1.x)), "r"(__double2hiint(m1.x)), "r"(__double2loint(m1.y)), "r"(__double2hiint(m1.y))
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double2 tm_m0(const uint32_t (&v)[8]) {
+  return make_double2(__hiloint2double(v[1], v[0]), __hiloint2double(v[3], v[2]));
+}
+__device__ __forceinline__ double2 tm_m1(const uint32_t (&v)[8]) {
+  return make_double2(__hiloint2double(v[5], v[4]), __hiloint2double(v[7], v[6]));
+}
+// TMEM column of M tile (strip b, tile t > b) of one frequency: strip b holds NT - 1 - b tiles
+__host__ __device__ constexpr int tm_tile(int NT, int b, int t) { return b * (NT - 1) - b * (b - 1) / 2 + (t - b - 1); }
 
 // B fragment (k = 4s + lane%4, n = lane/4) of an 8x8 tile held as C fragments (row lane/4, cols 2(lane%4) + {0,1})
 __device__ __forceinline__ double frag_c2b(double c0, double c1, int s, int lane) {
@@ -116,9 +148,10 @@ __device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double
 }
 
 // Column c, block b: Y_{b,c} = acc_b is final -> scratch (C-fragment order) and acc_t -= M_{t,b} Y_{b,c}, t > b.
-template <int NT, int B>
+// The M tiles come from shared memory, or (TM) from tensor memory: one tcgen05.ld per tile, one wait for all.
+template <int NT, int B, bool TM = false>
 __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S, double2 *gY,
-                                     int lane) {
+                                     int lane, uint32_t tm = 0) {
   gY[2 * lane] = make_double2(ar[B][0], ai[B][0]);
   gY[2 * lane + 1] = make_double2(ar[B][1], ai[B][1]);
   double nyr[2], yi[2], nyi[2];
@@ -130,12 +163,25 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], c
     nyi[s] = -i;
   }
   const int r4 = lane >> 2, q = lane & 3;
+  uint32_t v[NT][8];
+  if constexpr (TM) {
+#pragma unroll
+    for (int t = B + 1; t < NT; ++t) tm_ld8(tm + 8 * tm_tile(NT, B, t), v[t]);
+    tm_wait_ld();
+  }
   const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
-    const double2 *row = Sb + (8 * (t - B) + r4) * 8;
-    const double2 m0 = row[k0], m1 = row[k1];
+    double2 m0, m1;
+    if constexpr (TM) {
+      m0 = tm_m0(v[t]);
+      m1 = tm_m1(v[t]);
+    } else {
+      const double2 *row = Sb + (8 * (t - B) + r4) * 8;
+      m0 = row[k0];
+      m1 = row[k1];
+    }
     // acc -= M Y :  Re += Mr (-Yr) + Mi Yi ;  Im += Mr (-Yi) + Mi (-Yr)
     dmma(ar[t][0], ar[t][1], m0.x, nyr[0]);
     dmma(ai[t][0], ai[t][1], m0.x, nyi[0]);
@@ -148,18 +194,18 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], c
   }
 }
 
-template <int NT, int B = 0>
+template <int NT, bool TM = false, int B = 0>
 __device__ __forceinline__ void body_dispatch(int b, double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S,
-                                              double2 *gY, int lane) {
+                                              double2 *gY, int lane, uint32_t tm = 0) {
   if constexpr (B < NT - 1) {
-    if (b == B) body<NT, B>(ar, ai, S, gY, lane);
-    else body_dispatch<NT, B + 1>(b, ar, ai, S, gY, lane);
+    if (b == B) body<NT, B, TM>(ar, ai, S, gY, lane, tm);
+    else body_dispatch<NT, TM, B + 1>(b, ar, ai, S, gY, lane, tm);
   }
 }
 
 // Forward substitution z_t -= M_{t,B} z_B (real-ified right-hand side), t > B
-template <int NT, int B>
-__device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, int lane) {
+template <int NT, int B, bool TM = false>
+__device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, int lane, uint32_t tm = 0) {
   double b1[2], b2[2];
   rhs_frags(z[B][0], z[B][1], lane, b1, b2);
 #pragma unroll
@@ -168,12 +214,25 @@ __device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, i
     b2[s] = -b2[s];
   }
   const int r4 = lane >> 2, q = lane & 3;
+  uint32_t v[NT][8];
+  if constexpr (TM) {
+#pragma unroll
+    for (int t = B + 1; t < NT; ++t) tm_ld8(tm + 8 * tm_tile(NT, B, t), v[t]);
+    tm_wait_ld();
+  }
   const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
-    const double2 *row = Sb + (8 * (t - B) + r4) * 8;
-    const double2 m0 = row[k0], m1 = row[k1];
+    double2 m0, m1;
+    if constexpr (TM) {
+      m0 = tm_m0(v[t]);
+      m1 = tm_m1(v[t]);
+    } else {
+      const double2 *row = Sb + (8 * (t - B) + r4) * 8;
+      m0 = row[k0];
+      m1 = row[k1];
+    }
     dmma(z[t][0], z[t][1], m0.x, b1[0]);
     dmma(z[t][0], z[t][1], m0.y, b2[0]);
     dmma(z[t][0], z[t][1], m1.x, b1[1]);
@@ -196,11 +255,12 @@ __device__ __forceinline__ double2 afrag_cstore_s(const double2 *g, int s, int l
 // Unblocked LU with partial pivoting of panel c (rows 8c .. R-1 of strip c, lane = row), M_tc = L_tc L_cc^{-1},
 // interchanges applied to perm and to the strips of earlier panels.  Returns 0 or (LAPACK getrf info) k + 1 for
 // an exactly zero pivot column at global step k.
-template <int R, int MSE, bool PIVOT>
-__device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, double2 *gDiag, int lane) {
+template <int R, int MSE, bool PIVOT, bool TM = false>
+__device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, double2 *gDiag, int lane,
+                                     uint32_t tm = 0, int *sMap = nullptr) {
   constexpr int NT = R / 8;
   const int kb = 8 * c;
-  double2 *St = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, c) * 64;
+  double2 *St = TM ? S : S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, c) * 64;
   double2 pn[MSE][8], urc[MSE];
   int pos[MSE], q0[MSE], pv[MSE];
 #pragma unroll
@@ -288,6 +348,22 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
         for (int k = 0; k < 8; ++k) St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = pn[m][k];
       }
   }
+  if constexpr (TM) {
+    // diagonal block -> L2 scratch; the panel's M tiles (rows of tiles c+1..NT-1) -> tensor memory in A-fragment
+    // order (lane (r4, q) keeps M[r4][q] and M[r4][q + 4] of each tile); the shared-memory strip is then free
+    __syncwarp();
+    gDiag[c * 64 + 2 * lane] = St[2 * lane];
+    gDiag[c * 64 + 2 * lane + 1] = St[2 * lane + 1];
+    const int r4 = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int t = 1; t < NT; ++t)
+      if (t > c) {
+        const double2 *row = St + (8 * (t - c) + r4) * 8;
+        tm_st8(tm + 8 * tm_tile(NT, c, t), row[q ^ swz(r4)], row[(4 + q) ^ swz(r4)]);
+      }
+    tm_wait_st();
+    __syncwarp();
+  }
   // interchanges: perm and the rows [kb, R) of the strips of earlier panels follow the panel's row movement
   bool moved = false;
 #pragma unroll
@@ -296,30 +372,65 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
 #pragma unroll
     for (int m = 0; m < MSE; ++m)
       if (pos[m] < R && pos[m] != q0[m]) sPerm[pos[m]] = pv[m];
-    for (int b = 0; b < c; ++b) {
-      double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
+    if constexpr (TM) {
+      // row p (>= kb) of every earlier strip takes the old row sMap[p]: tiles c..NT-1 of strip b are read from
+      // tensor memory, laid out row-major in the (free) shared-memory strip, and written back permuted
+      const int r4 = lane >> 2, q = lane & 3;
+      for (int p = kb + lane; p < R; p += 32) sMap[p] = p;
+      __syncwarp();
 #pragma unroll
-      for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
-        double2 tmp[MSE][4];
+      for (int m = 0; m < MSE; ++m)
+        if (pos[m] < R && pos[m] != q0[m]) sMap[pos[m]] = q0[m];
+      __syncwarp();
+      for (int b = 0; b < c; ++b) {
+        uint32_t v[NT][8];
 #pragma unroll
-        for (int m = 0; m < MSE; ++m)
-          if (pos[m] < R && pos[m] != q0[m]) {
+        for (int t = 1; t < NT; ++t)
+          if (t >= c) tm_ld8(tm + 8 * tm_tile(NT, b, t), v[t]);
+        tm_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) tmp[m][k] = Sb[q0[m] * 8 + ((h + k) ^ swz(q0[m] & 7))];
+        for (int t = 1; t < NT; ++t)
+          if (t >= c) {
+            double2 *row = St + (8 * (t - c) + r4) * 8;
+            row[q] = tm_m0(v[t]);
+            row[4 + q] = tm_m1(v[t]);
           }
         __syncwarp();
 #pragma unroll
-        for (int m = 0; m < MSE; ++m)
-          if (pos[m] < R && pos[m] != q0[m]) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) Sb[pos[m] * 8 + ((h + k) ^ swz(pos[m] & 7))] = tmp[m][k];
+        for (int t = 1; t < NT; ++t)
+          if (t >= c) {
+            const double2 *src = St + (sMap[8 * t + r4] - kb) * 8;
+            tm_st8(tm + 8 * tm_tile(NT, b, t), src[q], src[4 + q]);
           }
+        tm_wait_st();
         __syncwarp();
+      }
+    } else {
+      for (int b = 0; b < c; ++b) {
+        double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
+#pragma unroll
+        for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
+          double2 tmp[MSE][4];
+#pragma unroll
+          for (int m = 0; m < MSE; ++m)
+            if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) tmp[m][k] = Sb[q0[m] * 8 + ((h + k) ^ swz(q0[m] & 7))];
+            }
+          __syncwarp();
+#pragma unroll
+          for (int m = 0; m < MSE; ++m)
+            if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) Sb[pos[m] * 8 + ((h + k) ^ swz(pos[m] & 7))] = tmp[m][k];
+            }
+          __syncwarp();
+        }
       }
     }
   }
   __syncwarp();
-  if constexpr (Cfg<R>::DIAG_L2) {
+  if constexpr (Cfg<R>::DIAG_L2 && !TM) {
     // the diagonal block (L_cc \ U_cc with 1/U_kk on the diagonal, swizzled rows) -> L2 scratch for the inverses;
     // its shared-memory tile is reused by the next strip
     gDiag[c * 64 + 2 * lane] = St[2 * lane];
@@ -335,10 +446,10 @@ namespace lull {
 
 // a2 + the left-looking updates of column tile c for one frequency: A[perm rows, c] = K + i s M gathered into C
 // fragments, minus sum_{b < c} M_{:,b} Y_{b,c} (DMMA), then rows >= 8c to the panel's virtual strip.
-template <int R>
+template <int R, bool TM = false>
 __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], double (&ai)[R / 8][2], double2 *S,
                                             double2 *gY, const int *sPerm, const double2 *gK, const double2 *gM,
-                                            double s, int lane, int ldkm = R) {
+                                            double s, int lane, int ldkm = R, uint32_t tm = 0) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
@@ -353,8 +464,8 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
     ai[tt][1] = fma(s, m1.x, k1.y);
   }
   if constexpr (!(PODP_LL_ABLATE & 2))
-    for (int b = 0; b < c; ++b) body_dispatch<NT>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane);
-  double2 *St = S + strip_off<C::DIAG_L2>(NT, c) * 64;
+    for (int b = 0; b < c; ++b) body_dispatch<NT, TM>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
+  double2 *St = TM ? S : S + strip_off<C::DIAG_L2>(NT, c) * 64;
 #pragma unroll
   for (int tt = 0; tt < NT; ++tt) {
     if (tt >= c) {
@@ -367,10 +478,10 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
 
 // After the factorisation of one frequency: z = P_perm B (real-ified: cols [Re b_0..2 | Im b_0..2 | 0 0]), forward
 // sweep, diagonal-block inverses D_t, block back substitution, P written (workspace and optional debug output).
-template <int R>
+template <int R, bool TM = false>
 __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, double om, const double2 *S,
                                        double2 *gY, double2 *gD, const double2 *gDiag, const int *sPerm, double *Pw,
-                                       int64_t t, int lane) {
+                                       int64_t t, int lane, uint32_t tm = 0) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
@@ -396,14 +507,15 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   }
   if constexpr (!(PODP_LL_ABLATE & 8))
     [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
-      (body_rhs<NT, Bs>(z, S, lane), ...);
+      (body_rhs<NT, Bs, TM>(z, S, lane, tm), ...);
     }(std::make_integer_sequence<int, NT - 1>{});
   // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----------
   // DIAG_L2: the strips are no longer needed after the forward sweep, so the diagonal blocks are brought back from
   // the L2 scratch into shared-memory tiles 0..NT-1 (one round of independent loads) and D_t goes to tiles
   // NT..2NT-1, where the back substitution reads it (no L2 round trips on either chain)
-  double2 *sD = const_cast<double2 *>(S) + NT * 64;
-  if constexpr (C::DIAG_L2) {
+  // (TM: the shared-memory strip has only NT tiles; D_t overwrites the staged blocks in place, see below)
+  double2 *sD = const_cast<double2 *>(S) + (TM ? 0 : NT * 64);
+  if constexpr (C::DIAG_L2 || TM) {
     __syncwarp();
     double2 *Sw = const_cast<double2 *>(S);
     for (int e = lane; e < NT * 64; e += 32) Sw[e] = __ldcg(gDiag + e);
@@ -414,9 +526,11 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
 #pragma unroll 1
     for (int t0 = 0; t0 < NT; t0 += 4) {
       const int td = t0 + (lane >> 3);
-      if (td < NT) {
-        // L\U diagonal block of panel td: staged copy (DIAG_L2) or rows 0..7 of strip td
-        const double2 *Dg = C::DIAG_L2 ? S + td * 64 : S + strip_off<false>(NT, td) * 64;
+      const bool act = td < NT;
+      const int tdc = act ? td : NT - 1;  // idle lanes recompute the last block (results discarded)
+      {
+        // L\U diagonal block of panel td: staged copy (DIAG_L2, TM) or rows 0..7 of strip td
+        const double2 *Dg = (C::DIAG_L2 || TM) ? S + tdc * 64 : S + strip_off<false>(NT, tdc) * 64;
         double2 y[8], x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -432,9 +546,12 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
           for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ swz(i))], x[k], acc);
           x[i] = cmul(acc, Dg[i * 8 + (i ^ swz(i))]);  // 1/U_ii (stored by the panel)
         }
-        double2 *dt = C::DIAG_L2 ? sD + td * 64 : gD + td * 64;
+        double2 *dt = (C::DIAG_L2 || TM) ? sD + tdc * 64 : gD + tdc * 64;
+        if constexpr (TM) __syncwarp();  // D_t overwrites the staged block it was computed from
+        if (act) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+          for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+        }
       }
     }
   }
@@ -444,8 +561,8 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   for (int tt = NT - 1; tt >= 0; --tt) {
     double b1[2], b2[2];
     rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
-    const double2 d0 = C::DIAG_L2 ? afrag_cstore_s(sD + tt * 64, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
-    const double2 d1 = C::DIAG_L2 ? afrag_cstore_s(sD + tt * 64, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
+    const double2 d0 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * 64, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
+    const double2 d1 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * 64, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
     double x0 = 0.0, x1 = 0.0;
     dmma(x0, x1, d0.x, b1[0]);
     dmma(x0, x1, d0.y, b2[0]);
@@ -498,15 +615,16 @@ __device__ __forceinline__ void fail_out(const EvalArgs &a, double *Pw, int R, i
 
 }  // namespace lull
 
-template <int R, bool PIVOT, bool KM>
-__global__ void __launch_bounds__(lull::Cfg<R, KM>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
-  using C = lull::Cfg<R, KM>;
+template <int R, bool PIVOT, bool KM, bool TM = false>
+__global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
+  using C = lull::Cfg<R, KM, TM>;
   constexpr int NT = C::NT, G = C::G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2 *S = reinterpret_cast<double2 *>(smem_raw + (size_t)wid * C::W_BYTES);
   double2 *sRow = S + C::STRIP_TILES * 64;
   int *sPerm = reinterpret_cast<int *>(sRow + 9);
+  int *sMap = sPerm + ((R + 3) / 4) * 4;  // TM: interchange source map (positions >= kb)
   const int64_t total = (int64_t)a.n_obj * a.F;
   const int64_t gw = (int64_t)blockIdx.x * G + wid, nw = (int64_t)gridDim.x * G;
   double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
@@ -521,13 +639,30 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM>::G * 32, 1) lu_ll_kernel(Eval
     ++obj;
   }
   double2 *sKM = reinterpret_cast<double2 *>(smem_raw + (size_t)G * C::W_BYTES);
-  if constexpr (KM) {  // single-object launch: K and M of object 0 into shared memory, once per CTA
+  if constexpr (C::KM_BYTES > 0) {  // single-object launch: K and M of object 0 into shared memory, once per CTA
     const double2 *k0p = reinterpret_cast<const double2 *>(a.ops + a.L.K), *m0p = reinterpret_cast<const double2 *>(a.ops + a.L.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
       const int i = e / R, j = e - i * R;
       sKM[i * (R + 1) + j] = __ldg(k0p + e);
       sKM[R * (R + 1) + i * (R + 1) + j] = __ldg(m0p + e);
     }
+  }
+  // TM: 512 TMEM columns for the CTA (warp 0 allocates and frees); warp w uses the lanes of its SM sub-partition
+  // (32 (w % 4) ..) and columns (w / 4) TM_COLS ..
+  __shared__ uint32_t s_tmem;
+  uint32_t tm = 0;
+  if constexpr (TM) {
+    if (wid == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&s_tmem))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tm = s_tmem + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((wid >> 2) * C::TM_COLS);
+  } else if constexpr (C::KM_BYTES > 0) {
     __syncthreads();
   }
   for (int64_t t = gw; t < total; t += nw) {
@@ -544,19 +679,19 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM>::G * 32, 1) lu_ll_kernel(Eval
       __syncwarp();
       double ar[NT][2], ai[NT][2];
       for (int c = 0; c < NT; ++c) {
-        lull::column_tile<R>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM);
+        lull::column_tile<R, TM>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM, tm);
         __syncwarp();
         if constexpr (PODP_LL_ABLATE & 1) {
           info = 0;
         } else if constexpr (C::MS > 1) {
-          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT>(c, S, sRow, sPerm, gDiag, lane)
-                                  : lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, gDiag, lane);
+          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap)
+                                  : lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap);
         } else {
-          info = lull::panel<R, 1, PIVOT>(c, S, sRow, sPerm, gDiag, lane);
+          info = lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap);
         }
         if (info != 0) break;
       }
-      if (info == 0) lull::finish<R>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane);
+      if (info == 0) lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm);
     }
     lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
@@ -566,13 +701,19 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM>::G * 32, 1) lu_ll_kernel(Eval
       ++obj;
     }
   }
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+  }
 }
 
 namespace lull {
-template <int R, bool KM>
+template <int R, bool KM, bool TM>
 static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
-  using C = Cfg<R, KM>;
-  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false, KM> : lu_ll_kernel<R, true, KM>;
+  using C = Cfg<R, KM, TM>;
+  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false, KM, TM> : lu_ll_kernel<R, true, KM, TM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)a.n_obj * a.F;
@@ -584,12 +725,17 @@ static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
 
 template <int R>
 static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
-  // K and M in shared memory only where it costs no warps (R <= 40) and the launch has one object
+  // single-object launches: K and M in shared memory -- directly where it costs no warps (R <= 40), with the M
+  // tiles in tensor memory for 40 < R <= 64
   if constexpr (R <= 40) {
     static_assert(Cfg<R, true>::G == Cfg<R, false>::G, "KM variant must keep the warp count");
-    if (a.n_obj == 1) return launch_k<R, true>(a, s, sms);
+    if (a.n_obj == 1) return launch_k<R, true, false>(a, s, sms);
+  } else if constexpr (R <= 64) {
+#ifndef PODP_LL_NO_TMEM
+    if (a.n_obj == 1) return launch_k<R, false, true>(a, s, sms);
+#endif
   }
-  return launch_k<R, false>(a, s, sms);
+  return launch_k<R, false, false>(a, s, sms);
 }
 }  // namespace lull
 
@@ -598,10 +744,15 @@ size_t lu_ll_scratch_bytes(int R, int sms) {
   const int NT = R / 8;
   int G = 0;
   switch (R) {
+#define PODP_CASE(RR)                                                                              \
+  case RR:                                                                                         \
+    G = lull::Cfg<RR>::G > lull::Cfg<RR, false, true>::G ? lull::Cfg<RR>::G : lull::Cfg<RR, false, true>::G; \
+    break;
+    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+#undef PODP_CASE
 #define PODP_CASE(RR) \
   case RR: G = lull::Cfg<RR>::G; break;
-    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
-    PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
 #undef PODP_CASE
     default: return 0;
   }
