@@ -56,7 +56,14 @@ __global__ void __launch_bounds__(mpttile::WARPS * 32, 1) mpt_tile_kernel(EvalAr
   int loaded_obj = -1;
   const double nanv = __longlong_as_double(0x7ff8000000000000ll);
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // Multi-object launches take a contiguous range of tiles per CTA (operators are re-staged only where the range
+  // crosses an object boundary, not on nearly every tile as with a round-robin assignment); one object: round robin.
+  const bool blocked = a.n_obj > 1;
+  const int64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t tile_begin = blocked ? (int64_t)blockIdx.x * per_cta : blockIdx.x;
+  const int64_t tile_end = blocked ? (tile_begin + per_cta < ntiles ? tile_begin + per_cta : ntiles) : ntiles;
+  const int64_t tile_step = blocked ? 1 : gridDim.x;
+  for (int64_t tile = tile_begin; tile < tile_end; tile += tile_step) {
     const int64_t t0 = tile * TILE;
     int64_t t = t0 + warp * FPW + fl;  // my frequency (global evaluation index)
     const bool valid = t < total;
