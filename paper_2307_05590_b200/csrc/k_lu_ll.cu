@@ -615,7 +615,7 @@ __device__ __forceinline__ void fail_out(const EvalArgs &a, double *Pw, int R, i
 
 }  // namespace lull
 
-template <int R, bool PIVOT, bool KM, bool TM = false>
+template <int R, bool PIVOT, bool KM, bool TM = false, bool SEG = false>
 __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(EvalArgs a) {
   using C = lull::Cfg<R, KM, TM>;
   constexpr int NT = C::NT, G = C::G;
@@ -631,22 +631,7 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
   double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
   double2 *gDiag = gD + NT * 64;  // L\U diagonal blocks (panel order)
 
-  // (obj, f) of evaluation t, advanced incrementally (no 64-bit division, whose subroutine call forces spills)
-  int obj = 0;
-  int64_t f = gw;
-  while (f >= a.F) {
-    f -= a.F;
-    ++obj;
-  }
   double2 *sKM = reinterpret_cast<double2 *>(smem_raw + (size_t)G * C::W_BYTES);
-  if constexpr (C::KM_BYTES > 0) {  // single-object launch: K and M of object 0 into shared memory, once per CTA
-    const double2 *k0p = reinterpret_cast<const double2 *>(a.ops + a.L.K), *m0p = reinterpret_cast<const double2 *>(a.ops + a.L.M);
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int i = e / R, j = e - i * R;
-      sKM[i * (R + 1) + j] = __ldg(k0p + e);
-      sKM[R * (R + 1) + i * (R + 1) + j] = __ldg(m0p + e);
-    }
-  }
   // TM: 512 TMEM columns for the CTA (warp 0 allocates and frees); warp w uses the lanes of its SM sub-partition
   // (32 (w % 4) ..) and columns (w / 4) TM_COLS ..
   __shared__ uint32_t s_tmem;
@@ -662,10 +647,10 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tm = s_tmem + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((wid >> 2) * C::TM_COLS);
-  } else if constexpr (C::KM_BYTES > 0) {
-    __syncthreads();
   }
-  for (int64_t t = gw; t < total; t += nw) {
+
+  // one evaluation t = (obj, f) by this warp
+  auto process = [&](int64_t t, int obj, int64_t f) {
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = a.omega[f];
     const double s = om * op[a.L.scal + SC_NU];
@@ -695,10 +680,55 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
     }
     lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
-    f += nw;
+  };
+
+  auto stage_km = [&](int obj) {  // K and M of one object into shared memory (row stride R + 1), whole CTA
+    const double2 *k0p = reinterpret_cast<const double2 *>(a.ops + (size_t)obj * a.L.stride + a.L.K);
+    const double2 *m0p = reinterpret_cast<const double2 *>(a.ops + (size_t)obj * a.L.stride + a.L.M);
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, j = e - i * R;
+      sKM[i * (R + 1) + j] = __ldg(k0p + e);
+      sKM[R * (R + 1) + i * (R + 1) + j] = __ldg(m0p + e);
+    }
+  };
+  if constexpr (SEG) {
+    // K and M in shared memory, several objects: the CTA takes a contiguous range of evaluations and walks it
+    // object by object, staging each object's K and M once (CTA-wide barriers only at object boundaries)
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t start = (int64_t)blockIdx.x * per, end = start + per < total ? start + per : total;
+    int64_t seg = start;
+    int obj = start < total ? (int)(start / a.F) : 0;
+    while (seg < end) {
+      const int64_t obj_end = (int64_t)(obj + 1) * a.F, seg_end = obj_end < end ? obj_end : end;
+      __syncthreads();  // every warp is done with the previous object's K and M
+      stage_km(obj);
+      __syncthreads();
+      const int64_t fbase = (int64_t)obj * a.F;
+      for (int64_t t = seg + wid; t < seg_end; t += G) process(t, obj, t - fbase);
+      seg = seg_end;
+      ++obj;
+    }
+  } else {
+    // round robin over the grid's warps (one object: its K and M staged once, if KM); (obj, f) of evaluation t
+    // advanced incrementally (no 64-bit division, whose subroutine call forces spills).  (Measured: for one object
+    // the round robin is faster than contiguous ranges per CTA, r = 64 5.80 vs 6.17 ms.)
+    if constexpr (C::KM_BYTES > 0) {
+      stage_km(0);
+      __syncthreads();
+    }
+    int obj = 0;
+    int64_t f = gw;
     while (f >= a.F) {
       f -= a.F;
       ++obj;
+    }
+    for (int64_t t = gw; t < total; t += nw) {
+      process(t, obj, f);
+      f += nw;
+      while (f >= a.F) {
+        f -= a.F;
+        ++obj;
+      }
     }
   }
   if constexpr (TM) {
@@ -713,7 +743,14 @@ namespace lull {
 template <int R, bool KM, bool TM>
 static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
   using C = Cfg<R, KM, TM>;
-  auto kern = (a.flags & PODP_FLAG_NO_PIVOT) ? lu_ll_kernel<R, false, KM, TM> : lu_ll_kernel<R, true, KM, TM>;
+  // K and M in shared memory: contiguous per-CTA ranges walked object by object (SEG) for several objects, and for
+  // one object at R <= 40 (measured: c1 solve 0.111 -> 0.104 ms); one object at 48 <= R <= 64 keeps the round robin
+  // (measured faster there: r = 64 5.80 vs 6.17 ms)
+  constexpr bool KMT = KM || TM;
+  const bool seg = KMT && (a.n_obj > 1 || KM);
+  auto kern = (a.flags & PODP_FLAG_NO_PIVOT)
+                  ? (seg ? lu_ll_kernel<R, false, KM, TM, KMT> : lu_ll_kernel<R, false, KM, TM, false>)
+                  : (seg ? lu_ll_kernel<R, true, KM, TM, KMT> : lu_ll_kernel<R, true, KM, TM, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   const int64_t total = (int64_t)a.n_obj * a.F;
@@ -725,14 +762,14 @@ static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
 
 template <int R>
 static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
-  // single-object launches: K and M in shared memory -- directly where it costs no warps (R <= 40), with the M
-  // tiles in tensor memory for 40 < R <= 64
+  // K and M in shared memory (per object, contiguous evaluation ranges per CTA) -- directly where it costs no warps
+  // (R <= 40), with the M tiles in tensor memory for 40 < R <= 64
   if constexpr (R <= 40) {
     static_assert(Cfg<R, true>::G == Cfg<R, false>::G, "KM variant must keep the warp count");
-    if (a.n_obj == 1) return launch_k<R, true, false>(a, s, sms);
+    return launch_k<R, true, false>(a, s, sms);
   } else if constexpr (R <= 64) {
 #ifndef PODP_LL_NO_TMEM
-    if (a.n_obj == 1) return launch_k<R, false, true>(a, s, sms);
+    return launch_k<R, false, true>(a, s, sms);
 #endif
   }
   return launch_k<R, false, false>(a, s, sms);
