@@ -69,7 +69,12 @@ enum {
   PODP_FLAG_LU_LL = 1u << 8,      /* left-looking block LU, one warp per frequency, padded r <= 96 (k_lu_ll.cu) */
   PODP_FLAG_LU_BLK = 1u << 9,     /* lock-step panel-blocked LU, W warps per frequency, padded r <= 96        */
   PODP_FLAG_LU_DYN = 1u << 10,    /* dynamically scheduled blocked LU, W warps per frequency, padded r <= 96  */
-  PODP_FLAG_LU_GENERIC = 1u << 11 /* generic one-warp LU (any r <= 128, pivoting or PODP_FLAG_NO_PIVOT)       */
+  PODP_FLAG_LU_GENERIC = 1u << 11, /* generic one-warp LU (any r <= 128, pivoting or PODP_FLAG_NO_PIVOT)      */
+  /* Measurement only (A/B of the contraction design): the MPT / certificate forms as FP64 tensor-core GEMMs over the
+     solution panel with bulk-copy (TMA) staging (k_mpt_gemm.cu) instead of the default operator-stationary kernel;
+     one object, padded r in {24, 48, 96}, not with PODP_FLAG_PENCIL (else PODP_ERR_UNSUPPORTED).  Same results up
+     to rounding. */
+  PODP_FLAG_MPT_GEMM = 1u << 13
 };
 
 /* Operators of ONE object (host pointers; copied, validated and packed by podp_create; caller keeps ownership).

@@ -52,6 +52,7 @@ cudaError_t launch_lu_blk(const EvalArgs &a, cudaStream_t s);
 cudaError_t launch_lu_dyn(const EvalArgs &a, cudaStream_t s);
 size_t lu_dyn_scratch_bytes(int R, int sms);                          // right-hand-side scratch of its RG mode
 cudaError_t launch_mpt_tile(const EvalArgs &a, cudaStream_t s, bool diag = false);
+cudaError_t launch_mpt_gemm(const EvalArgs &a, cudaStream_t s, int sms);  // A/B: DMMA GEMM + bulk-copy variant
 cudaError_t launch_pencil(const EvalArgs &a, cudaStream_t s);    // N3 pencil solve (P only)
 cudaError_t launch_pencil_y(const EvalArgs &a, cudaStream_t s);  // N3: y = (I + i s Lambda)^{-1}(c0 + omega c1) only
 cudaError_t launch_invariants(const double *T1, const double *I, int64_t n, double *eigR, double *eigI, cudaStream_t s);

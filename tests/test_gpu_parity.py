@@ -557,3 +557,23 @@ def test_batch_objects_every_lu_path(torch_cuda, r):
         alone = run_gpu(torch, [ops[k]], omega)
         for q in ("T1", "I", "Delta"):
             assert np.array_equal(np.nan_to_num(alone[q][0]).view(np.uint64), np.nan_to_num(res[q][k]).view(np.uint64)), (k, q)
+
+
+@pytest.mark.parametrize("r,F", [(24, 333), (48, 257), (96, 61), (20, 49)])
+def test_mpt_gemm_variant_parity(torch_cuda, r, F):
+    """A/B variant of the contraction (PODP_FLAG_MPT_GEMM: DMMA GEMMs over the solution panel, bulk-copy staging):
+    per-entry parity against the oracle, including a ragged last tile; unsupported cases are refused."""
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_MPT_GEMM, FLAG_OUT_R, PodpError
+    ops = g.make_operators(r)
+    omega = g.omega_grid(F)
+    if (r + 7) // 8 * 8 not in (24, 48, 96):
+        ev = Evaluator(ops)
+        with pytest.raises(PodpError) as ei:
+            ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_MPT_GEMM)
+        assert ei.value.status == 4
+        ev.close()
+        return
+    res = run_gpu(torch, ops, omega, flags=FLAG_OUT_R | FLAG_MPT_GEMM)
+    assert (res["info"] == 0).all()
+    check_parity(ops, omega, res)
