@@ -52,14 +52,24 @@ struct Cfg {
   // 8-column slice per tile in A-fragment order, this warp's 32 TMEM lanes); shared memory keeps only the current
   // panel's virtual strip (NT tiles, also the scratch of the row interchanges and of the final inverses), so K and M
   // fit in shared memory beside 12 warps' state (KM)
-  static constexpr int TM_TILES = NT * (NT - 1) / 2;     // M tiles per frequency (8 TMEM columns each)
-  static constexpr int STRIP_TILES = TM ? NT : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
+  // strips 0 .. TM_TB-1 live in tensor memory; at R = 96 the last strips (TM_TB .. NT-2) do not fit in this warp's
+  // 512 columns and stay in shared memory after the virtual strip
+  static constexpr int tm_tiles(int tb) { return tb * (NT - 1) - tb * (tb - 1) / 2; }
+  static constexpr int tm_fit() {
+    int tb = 0;
+    while (tb < NT - 1 && 8 * tm_tiles(tb + 1) <= 512) ++tb;
+    return tb;
+  }
+  static constexpr int TM_TB = TM ? tm_fit() : 0;
+  static constexpr int TM_TILES = tm_tiles(TM_TB);       // M tiles per frequency in TMEM (8 columns each)
+  static constexpr int HYB_TILES = NT * (NT - 1) / 2 - TM_TILES;
+  static constexpr int STRIP_TILES = TM ? NT + HYB_TILES : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
   static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16 * (TM ? 2 : 1);
   // KM (single-object launches, R <= 40, or with TM): K and M staged once per CTA in shared memory (row stride
   // R + 1 complex), so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 ->
   // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
-  static constexpr int KM_BYTES = (KM || TM) ? 2 * R * (R + 1) * 16 : 0;
+  static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? 2 * R * (R + 1) * 16 : 0;
   static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
   // warp cap (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition, 224-255
   // above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
@@ -69,9 +79,11 @@ struct Cfg {
 #else
   static constexpr int G_MAX = G_REG;
 #endif
-  static constexpr int G = G_SMEM < G_MAX ? G_SMEM : G_MAX;  // warps (= concurrent frequencies) per CTA
-  // TMEM columns per warp (power-of-two stride so each of the (G + 3) / 4 warps of a sub-partition gets a slice)
-  static constexpr int TM_COLS = 8 * TM_TILES <= 64 ? 64 : (8 * TM_TILES <= 128 ? 128 : 256);
+  // TMEM columns per warp (power-of-two stride so each of the warps of a sub-partition gets a slice)
+  static constexpr int TM_COLS = 8 * TM_TILES <= 64 ? 64 : (8 * TM_TILES <= 128 ? 128 : (8 * TM_TILES <= 256 ? 256 : 512));
+  static constexpr int G_TM = TM ? 4 * (512 / TM_COLS) : 64;
+  static constexpr int G_SR = G_SMEM < G_MAX ? G_SMEM : G_MAX;
+  static constexpr int G = G_SR < G_TM ? G_SR : G_TM;    // warps (= concurrent frequencies) per CTA
   static_assert(!TM || TM_COLS * ((G + 3) / 4) <= 512, "M tiles do not fit in tensor memory");
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
   static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
@@ -85,6 +97,11 @@ struct Cfg {
 // only), so the diagonal-block tile of panel b is the last tile of strip b+1 (or the spare tile): space that is
 // written only after panel b has copied its diagonal block to the L2 scratch.  Every access to the M tiles of strip
 // b is at tile offset >= 1 from strip_off(b), in both layouts.
+// TM, strips b >= TB kept in shared memory (R = 96): strip b's virtual base sits so that its tile t is at tile
+// NT + (tiles of strips TB .. b-1) + (t - b - 1), i.e. base = NT - 1 + sum_{TB <= b' < b} (NT - 1 - b')
+__host__ __device__ constexpr int strip_off_hyb(int NT, int TB, int b) {
+  return NT - 1 + (b - TB) * (NT - 1) - (b * (b - 1) - TB * (TB - 1)) / 2;
+}
 template <bool DIAG_L2>
 __host__ __device__ constexpr int strip_off(int NT, int b) {
   return DIAG_L2 ? (NT - 2 - b) * (NT - 1 - b) / 2 : b * NT - b * (b - 1) / 2;
@@ -163,18 +180,24 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], c
     nyi[s] = -i;
   }
   const int r4 = lane >> 2, q = lane & 3;
+  constexpr int TB = Cfg<8 * NT, false, TM>::TM_TB;
+  constexpr bool IN_TM = TM && B < TB;  // this strip in tensor memory (else shared memory)
+  // TMEM loads in chunks of TMC tiles (one wait per chunk) to bound the registers they occupy
+  constexpr int TMC = 4;
   uint32_t v[NT][8];
-  if constexpr (TM) {
-#pragma unroll
-    for (int t = B + 1; t < NT; ++t) tm_ld8(tm + 8 * tm_tile(NT, B, t), v[t]);
-    tm_wait_ld();
-  }
-  const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
+  const double2 *Sb = S + (TM ? strip_off_hyb(NT, TB, B) : strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B)) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
+    if constexpr (IN_TM) {
+      if ((t - B - 1) % TMC == 0) {
+#pragma unroll
+        for (int u = t; u < NT && u < t + TMC; ++u) tm_ld8(tm + 8 * tm_tile(NT, B, u), v[u]);
+        tm_wait_ld();
+      }
+    }
     double2 m0, m1;
-    if constexpr (TM) {
+    if constexpr (IN_TM) {
       m0 = tm_m0(v[t]);
       m1 = tm_m1(v[t]);
     } else {
@@ -214,18 +237,24 @@ __device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, i
     b2[s] = -b2[s];
   }
   const int r4 = lane >> 2, q = lane & 3;
+  constexpr int TB = Cfg<8 * NT, false, TM>::TM_TB;
+  constexpr bool IN_TM = TM && B < TB;  // this strip in tensor memory (else shared memory)
+  // TMEM loads in chunks of TMC tiles (one wait per chunk) to bound the registers they occupy
+  constexpr int TMC = 4;
   uint32_t v[NT][8];
-  if constexpr (TM) {
-#pragma unroll
-    for (int t = B + 1; t < NT; ++t) tm_ld8(tm + 8 * tm_tile(NT, B, t), v[t]);
-    tm_wait_ld();
-  }
-  const double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B) * 64;
+  const double2 *Sb = S + (TM ? strip_off_hyb(NT, TB, B) : strip_off<Cfg<8 * NT>::DIAG_L2>(NT, B)) * 64;
   const int k0 = q ^ swz(r4), k1 = (4 + q) ^ swz(r4);
 #pragma unroll
   for (int t = B + 1; t < NT; ++t) {
+    if constexpr (IN_TM) {
+      if ((t - B - 1) % TMC == 0) {
+#pragma unroll
+        for (int u = t; u < NT && u < t + TMC; ++u) tm_ld8(tm + 8 * tm_tile(NT, B, u), v[u]);
+        tm_wait_ld();
+      }
+    }
     double2 m0, m1;
-    if constexpr (TM) {
+    if constexpr (IN_TM) {
       m0 = tm_m0(v[t]);
       m1 = tm_m1(v[t]);
     } else {
@@ -355,13 +384,19 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     gDiag[c * 64 + 2 * lane] = St[2 * lane];
     gDiag[c * 64 + 2 * lane + 1] = St[2 * lane + 1];
     const int r4 = lane >> 2, q = lane & 3;
+    constexpr int TB = Cfg<R, false, TM>::TM_TB;
+    if (c < TB) {
 #pragma unroll
-    for (int t = 1; t < NT; ++t)
-      if (t > c) {
-        const double2 *row = St + (8 * (t - c) + r4) * 8;
-        tm_st8(tm + 8 * tm_tile(NT, c, t), row[q ^ swz(r4)], row[(4 + q) ^ swz(r4)]);
-      }
-    tm_wait_st();
+      for (int t = 1; t < NT; ++t)
+        if (t > c) {
+          const double2 *row = St + (8 * (t - c) + r4) * 8;
+          tm_st8(tm + 8 * tm_tile(NT, c, t), row[q ^ swz(r4)], row[(4 + q) ^ swz(r4)]);
+        }
+      tm_wait_st();
+    } else {  // (R = 96) strips TB.. stay in shared memory, after the virtual strip
+      double2 *dst = S + strip_off_hyb(NT, TB, c) * 64;
+      for (int e = 64 + lane; e < (NT - c) * 64; e += 32) dst[e] = St[e];
+    }
     __syncwarp();
   }
   // interchanges: perm and the rows [kb, R) of the strips of earlier panels follow the panel's row movement
@@ -372,9 +407,31 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
 #pragma unroll
     for (int m = 0; m < MSE; ++m)
       if (pos[m] < R && pos[m] != q0[m]) sPerm[pos[m]] = pv[m];
+    // shared-memory strips: swap the moved rows in place (row i of strip b at Sb + 8 i)
+    auto swap_rows_smem = [&](double2 *Sb) {
+#pragma unroll
+      for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
+        double2 tmp[MSE][4];
+#pragma unroll
+        for (int m = 0; m < MSE; ++m)
+          if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tmp[m][k] = Sb[q0[m] * 8 + ((h + k) ^ swz(q0[m] & 7))];
+          }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < MSE; ++m)
+          if (pos[m] < R && pos[m] != q0[m]) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) Sb[pos[m] * 8 + ((h + k) ^ swz(pos[m] & 7))] = tmp[m][k];
+          }
+        __syncwarp();
+      }
+    };
     if constexpr (TM) {
       // row p (>= kb) of every earlier strip takes the old row sMap[p]: tiles c..NT-1 of strip b are read from
       // tensor memory, laid out row-major in the (free) shared-memory strip, and written back permuted
+      constexpr int TB = Cfg<R, false, TM>::TM_TB;
       const int r4 = lane >> 2, q = lane & 3;
       for (int p = kb + lane; p < R; p += 32) sMap[p] = p;
       __syncwarp();
@@ -383,50 +440,30 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
         if (pos[m] < R && pos[m] != q0[m]) sMap[pos[m]] = q0[m];
       __syncwarp();
       for (int b = 0; b < c; ++b) {
-        uint32_t v[NT][8];
-#pragma unroll
-        for (int t = 1; t < NT; ++t)
-          if (t >= c) tm_ld8(tm + 8 * tm_tile(NT, b, t), v[t]);
-        tm_wait_ld();
-#pragma unroll
-        for (int t = 1; t < NT; ++t)
-          if (t >= c) {
-            double2 *row = St + (8 * (t - c) + r4) * 8;
-            row[q] = tm_m0(v[t]);
-            row[4 + q] = tm_m1(v[t]);
-          }
+        if (b >= TB) {
+          swap_rows_smem(S + strip_off_hyb(NT, TB, b) * 64 - 8 * 8 * b);
+          continue;
+        }
+#pragma unroll 1
+        for (int t = c; t < NT; ++t) {  // one tile at a time (registers)
+          uint32_t v[8];
+          tm_ld8(tm + 8 * tm_tile(NT, b, t), v);
+          tm_wait_ld();
+          double2 *row = St + (8 * (t - c) + r4) * 8;
+          row[q] = tm_m0(v);
+          row[4 + q] = tm_m1(v);
+        }
         __syncwarp();
-#pragma unroll
-        for (int t = 1; t < NT; ++t)
-          if (t >= c) {
-            const double2 *src = St + (sMap[8 * t + r4] - kb) * 8;
-            tm_st8(tm + 8 * tm_tile(NT, b, t), src[q], src[4 + q]);
-          }
+#pragma unroll 1
+        for (int t = c; t < NT; ++t) {
+          const double2 *src = St + (sMap[8 * t + r4] - kb) * 8;
+          tm_st8(tm + 8 * tm_tile(NT, b, t), src[q], src[4 + q]);
+        }
         tm_wait_st();
         __syncwarp();
       }
     } else {
-      for (int b = 0; b < c; ++b) {
-        double2 *Sb = S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, b) * 64 - 8 * 8 * b;  // row i of strip b at Sb + 8 i
-#pragma unroll
-        for (int h = 0; h < 8; h += 4) {  // 4 columns at a time: all reads of a column precede its writes
-          double2 tmp[MSE][4];
-#pragma unroll
-          for (int m = 0; m < MSE; ++m)
-            if (pos[m] < R && pos[m] != q0[m]) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) tmp[m][k] = Sb[q0[m] * 8 + ((h + k) ^ swz(q0[m] & 7))];
-            }
-          __syncwarp();
-#pragma unroll
-          for (int m = 0; m < MSE; ++m)
-            if (pos[m] < R && pos[m] != q0[m]) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) Sb[pos[m] * 8 + ((h + k) ^ swz(pos[m] & 7))] = tmp[m][k];
-            }
-          __syncwarp();
-        }
-      }
+      for (int b = 0; b < c; ++b) swap_rows_smem(S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, b) * 64 - 8 * 8 * b);
     }
   }
   __syncwarp();
@@ -746,7 +783,7 @@ static cudaError_t launch_k(const EvalArgs &a, cudaStream_t s, int sms) {
   // K and M in shared memory: contiguous per-CTA ranges walked object by object (SEG) for several objects, and for
   // one object at R <= 40 (measured: c1 solve 0.111 -> 0.104 ms); one object at 48 <= R <= 64 keeps the round robin
   // (measured faster there: r = 64 5.80 vs 6.17 ms)
-  constexpr bool KMT = KM || TM;
+  constexpr bool KMT = C::KM_BYTES > 0;
   const bool seg = KMT && (a.n_obj > 1 || KM);
   auto kern = (a.flags & PODP_FLAG_NO_PIVOT)
                   ? (seg ? lu_ll_kernel<R, false, KM, TM, KMT> : lu_ll_kernel<R, false, KM, TM, false>)
@@ -767,8 +804,9 @@ static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
   if constexpr (R <= 40) {
     static_assert(Cfg<R, true>::G == Cfg<R, false>::G, "KM variant must keep the warp count");
     return launch_k<R, true, false>(a, s, sms);
-  } else if constexpr (R <= 64) {
+  } else if constexpr (R <= 64 || R == 96) {
 #ifndef PODP_LL_NO_TMEM
+    // (R = 96: strips 0..8 in tensor memory, the last two in shared memory; 4 warps per SM instead of 3)
     return launch_k<R, false, true>(a, s, sms);
 #endif
   }
@@ -785,11 +823,11 @@ size_t lu_ll_scratch_bytes(int R, int sms) {
   case RR:                                                                                         \
     G = lull::Cfg<RR>::G > lull::Cfg<RR, false, true>::G ? lull::Cfg<RR>::G : lull::Cfg<RR, false, true>::G; \
     break;
-    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64) PODP_CASE(96)
 #undef PODP_CASE
 #define PODP_CASE(RR) \
   case RR: G = lull::Cfg<RR>::G; break;
-    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88)
 #undef PODP_CASE
     default: return 0;
   }
