@@ -52,15 +52,34 @@ struct Cfg {
   // 8-column slice per tile in A-fragment order, this warp's 32 TMEM lanes); shared memory keeps only the current
   // panel's virtual strip (NT tiles, also the scratch of the row interchanges and of the final inverses), so K and M
   // fit in shared memory beside 12 warps' state (KM)
-  // strips 0 .. TM_TB-1 live in tensor memory; at R = 96 the last strips (TM_TB .. NT-2) do not fit in this warp's
-  // 512 columns and stay in shared memory after the virtual strip
+  // strips 0 .. TM_TB-1 live in tensor memory (TM_COLS columns per warp, 512 / TM_COLS warps per SM sub-partition);
+  // the remaining strips stay in shared memory after the virtual strip.  TM_COLS is chosen to maximise the warps per
+  // SM under the shared-memory, register and tensor-memory limits (r = 48: all 15 tiles in 128 columns, 12 warps;
+  // r = 80: 4 strips in 256 columns, 8 warps instead of 4; r = 96: 9 strips in 512 columns, 4 instead of 3)
   static constexpr int tm_tiles(int tb) { return tb * (NT - 1) - tb * (tb - 1) / 2; }
-  static constexpr int tm_fit() {
+  static constexpr int tm_fit(int cols) {
     int tb = 0;
-    while (tb < NT - 1 && 8 * tm_tiles(tb + 1) <= 512) ++tb;
+    while (tb < NT - 1 && 8 * tm_tiles(tb + 1) <= cols) ++tb;
     return tb;
   }
-  static constexpr int TM_TB = TM ? tm_fit() : 0;
+  static constexpr int PERM_BYTES = ((R * 4 + 15) / 16) * 16;
+  static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);  // register cap, see below
+  static constexpr int tm_warps(int cols) {
+    const int hyb = NT * (NT - 1) / 2 - tm_tiles(tm_fit(cols));
+    const int w_bytes = (NT + hyb) * 1024 + 9 * 16 + 2 * PERM_BYTES;
+    const int km = R <= 64 ? 2 * R * (R + 1) * 16 : 0;
+    const int g_smem = (227 * 1024 - km) / w_bytes, g_tm = 4 * (512 / cols);
+    const int g = g_smem < G_REG ? g_smem : G_REG;
+    return g < g_tm ? g : g_tm;
+  }
+  static constexpr int tm_best_cols() {
+    int best = 512;
+    for (int cols = 256; cols >= 64; cols /= 2)
+      if (tm_warps(cols) > tm_warps(best)) best = cols;
+    return best;
+  }
+  static constexpr int TM_COLS = TM ? tm_best_cols() : 64;
+  static constexpr int TM_TB = TM ? tm_fit(TM_COLS) : 0;
   static constexpr int TM_TILES = tm_tiles(TM_TB);       // M tiles per frequency in TMEM (8 columns each)
   static constexpr int HYB_TILES = NT * (NT - 1) / 2 - TM_TILES;
   static constexpr int STRIP_TILES = TM ? NT + HYB_TILES : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
@@ -71,16 +90,13 @@ struct Cfg {
   // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
   static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? 2 * R * (R + 1) * 16 : 0;
   static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
-  // warp cap (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition, 224-255
-  // above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
-  static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);
+  // warp cap G_REG (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition,
+  // 224-255 above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
 #ifdef PODP_LL_G  // dev: fewer warps per CTA (occupancy experiments)
   static constexpr int G_MAX = R <= 48 ? PODP_LL_G : G_REG;
 #else
   static constexpr int G_MAX = G_REG;
 #endif
-  // TMEM columns per warp (power-of-two stride so each of the warps of a sub-partition gets a slice)
-  static constexpr int TM_COLS = 8 * TM_TILES <= 64 ? 64 : (8 * TM_TILES <= 128 ? 128 : (8 * TM_TILES <= 256 ? 256 : 512));
   static constexpr int G_TM = TM ? 4 * (512 / TM_COLS) : 64;
   static constexpr int G_SR = G_SMEM < G_MAX ? G_SMEM : G_MAX;
   static constexpr int G = G_SR < G_TM ? G_SR : G_TM;    // warps (= concurrent frequencies) per CTA
@@ -804,10 +820,10 @@ static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
   if constexpr (R <= 40) {
     static_assert(Cfg<R, true>::G == Cfg<R, false>::G, "KM variant must keep the warp count");
     return launch_k<R, true, false>(a, s, sms);
-  } else if constexpr (R <= 64 || R == 96) {
+  } else {
 #ifndef PODP_LL_NO_TMEM
-    // (R = 96: strips 0..8 in tensor memory, the last two in shared memory; 4 warps per SM instead of 3)
-    return launch_k<R, false, true>(a, s, sms);
+    // tensor memory where it buys warps (or, up to R = 64, K and M in shared memory)
+    if constexpr (R <= 64 || Cfg<R, false, true>::G > Cfg<R, false, false>::G) return launch_k<R, false, true>(a, s, sms);
 #endif
   }
   return launch_k<R, false, false>(a, s, sms);
@@ -823,11 +839,11 @@ size_t lu_ll_scratch_bytes(int R, int sms) {
   case RR:                                                                                         \
     G = lull::Cfg<RR>::G > lull::Cfg<RR, false, true>::G ? lull::Cfg<RR>::G : lull::Cfg<RR, false, true>::G; \
     break;
-    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64) PODP_CASE(96)
+    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
 #undef PODP_CASE
 #define PODP_CASE(RR) \
   case RR: G = lull::Cfg<RR>::G; break;
-    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88)
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32)
 #undef PODP_CASE
     default: return 0;
   }
