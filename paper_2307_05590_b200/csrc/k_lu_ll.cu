@@ -88,7 +88,8 @@ struct Cfg {
   // KM (single-object launches, R <= 40, or with TM): K and M staged once per CTA in shared memory (row stride
   // R + 1 complex), so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 ->
   // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
-  static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? 2 * R * (R + 1) * 16 : 0;
+  // (+ b0 and b1, 3R complex each, read by the right-hand-side assembly of every frequency)
+  static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? (2 * R * (R + 1) + 6 * R) * 16 : 0;
   static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
   // warp cap G_REG (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition,
   // 224-255 above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
@@ -126,6 +127,11 @@ __host__ __device__ constexpr int strip_off(int NT, int b) {
 // 2j+1 x 4 consecutive k) hit 8 distinct 16-byte bank groups
 __device__ __forceinline__ int swz(int i) { return ((i & 1) << 2) | ((i >> 1) & 3); }
 
+__device__ __forceinline__ double selp_f64(double a, double b, int p) {  // p ? a : b
+  double r;
+  asm("{\n .reg .pred q;\n setp.ne.s32 q, %3, 0;\n selp.f64 %0, %1, %2, q;\n}" : "=d"(r) : "d"(a), "d"(b), "r"(p));
+  return r;
+}
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -308,6 +314,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
   double2 *St = TM ? S : S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, c) * 64;
   double2 pn[MSE][8], urc[MSE];
   int pos[MSE], q0[MSE], pv[MSE];
+  bool alive[MSE];  // not yet chosen as a pivot row (and a real row)
 #pragma unroll
   for (int m = 0; m < MSE; ++m) {
     const int i = kb + lane + 32 * m;
@@ -315,55 +322,104 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     q0[m] = i;
     pos[m] = v ? i : (1 << 20);
     pv[m] = v ? sPerm[i] : 0;
+    alive[m] = v;
 #pragma unroll
     for (int k = 0; k < 8; ++k) pn[m][k] = v ? St[(i - kb) * 8 + (k ^ swz(i & 7))] : make_double2(0.0, 0.0);
   }
+  // Column step j.  Rows never move between lanes.  R >= 48: strip row h = slot (lane + 32 m) of the panel holds
+  // that slot's current values, rewritten by its lane before each step (at j = 0 the strip already holds them), so
+  // the pivot row is read straight from the strip once the argmax is known; its reciprocal (computed speculatively
+  // by every candidate) and its position come by shuffle from the owning lane; the argmax key carries the slot
+  // (ties: lowest slot).  R <= 40 (SROW): the pivot row's owner copies it to the 9-entry sRow and the key carries
+  // the position (ties: lowest position) -- fewer shared-memory wavefronts, measured faster where 16 warps share
+  // them (r = 24 .. 40: 1.5-3 %; R >= 48 the other way round, r = 64: 3 %).
+  constexpr bool SROW = R <= 40;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int kr = kb + j;
+    if (!SROW && j > 0) {
+#pragma unroll
+      for (int m = 0; m < MSE; ++m)
+        if (alive[m]) {
+          const int h = lane + 32 * m;
+#pragma unroll
+          for (int k = j + 1; k < 8; ++k) St[h * 8 + (k ^ swz(h & 7))] = pn[m][k];
+        }
+    }
     unsigned key = 0u;
     double2 rcm[MSE];
 #pragma unroll
     for (int m = 0; m < MSE; ++m) {
-      const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | (unsigned)(127 - (pos[m] & 127));
+      const unsigned tie = SROW ? (unsigned)(127 - (pos[m] & 127)) : (unsigned)(127 - lane - 32 * m);
+      const unsigned kk = (mag_key_hi(pn[m][j]) & 0xFFFFFF80u) | tie;
       // candidates: every remaining row (partial pivoting) or only the row at position kr (PODP_FLAG_NO_PIVOT)
-      if ((PIVOT ? pos[m] >= kr : pos[m] == kr) && pos[m] < R && kk > key) key = kk;
+      if ((PIVOT ? alive[m] : pos[m] == kr) && kk > key) key = kk;
       if constexpr (PODP_LL_ABLATE & 64) rcm[m] = make_double2(1.0, 0.0);
       else rcm[m] = crecip_fast(pn[m][j]);  // speculative: off the chain after the argmax
     }
+    if constexpr (!SROW) __syncwarp();  // the strip rows written above are visible to the warp
     const unsigned best = __reduce_max_sync(0xffffffffu, key);
     if ((best >> 7) == 0u) return kr + 1;
-    const int p = 127 - (int)(best & 127u);
+    double2 rc, u[8];
+    int p;
+    bool piv[MSE];
+    if constexpr (SROW) {
+      p = 127 - (int)(best & 127u);
 #pragma unroll
-    for (int m = 0; m < MSE; ++m) {
-      if (pos[m] == p) {
-        const double d = fma(pn[m][j].x, pn[m][j].x, pn[m][j].y * pn[m][j].y);
-        sRow[8] = (d >= 1e-290 && d <= 1e290) ? rcm[m] : crecip_scaled(pn[m][j]);  // call-free slow path
+      for (int m = 0; m < MSE; ++m) {
+        piv[m] = pos[m] == p;
+        if (piv[m]) {
+          const double d = fma(pn[m][j].x, pn[m][j].x, pn[m][j].y * pn[m][j].y);
+          sRow[8] = (d >= 1e-290 && d <= 1e290) ? rcm[m] : crecip_scaled(pn[m][j]);  // call-free slow path
 #pragma unroll
-        for (int k = j + 1; k < 8; ++k) sRow[k] = pn[m][k];
+          for (int k = j + 1; k < 8; ++k) sRow[k] = pn[m][k];
+        }
       }
-    }
-    __syncwarp();
-    const double2 rc = sRow[8];
-    double2 u[8];
+      __syncwarp();
+      rc = sRow[8];
 #pragma unroll
-    for (int k = j + 1; k < 8; ++k) u[k] = sRow[k];
+      for (int k = j + 1; k < 8; ++k) u[k] = sRow[k];
+    } else {
+      const int ph = 127 - (int)(best & 127u), pl = ph & 31;
+      // pivot reciprocal: crecip_fast is exact to ~1 ulp while max(|Re|,|Im|) is in [2^-480, 2^478) (|z|^2
+      // normal); outside (warp-uniform, decided from the key's exponent bits) it is recomputed with crecip_scaled
+      if (const unsigned bh = best & 0xFFFFFF80u; bh < 0x21F00000u || bh >= 0x5DD00000u) {
+#pragma unroll
+        for (int m = 0; m < MSE; ++m) rcm[m] = crecip_scaled(pn[m][j]);  // call-free slow path
+      }
+      double2 rsrc = rcm[0];
+      int psrc = pos[0];
+#pragma unroll
+      for (int m = 1; m < MSE; ++m) {  // opaque selects: never an indexed local array
+        const int sel = (ph >> 5) == m;
+        rsrc = make_double2(selp_f64(rcm[m].x, rsrc.x, sel), selp_f64(rcm[m].y, rsrc.y, sel));
+        psrc = sel ? pos[m] : psrc;
+      }
+      rc = make_double2(__shfl_sync(0xffffffffu, rsrc.x, pl), __shfl_sync(0xffffffffu, rsrc.y, pl));
+      p = __shfl_sync(0xffffffffu, psrc, pl);
+#pragma unroll
+      for (int k = j + 1; k < 8; ++k) u[k] = St[ph * 8 + (k ^ swz(ph & 7))];
+#pragma unroll
+      for (int m = 0; m < MSE; ++m) piv[m] = lane + 32 * m == ph;
+    }
 #pragma unroll
     for (int m = 0; m < MSE; ++m) {
-      pos[m] = pos[m] == p ? kr : (pos[m] == kr ? p : pos[m]);
-      if (pos[m] == kr) urc[m] = rc;  // 1/U_kk, kept for the diagonal-block inverse
+      pos[m] = piv[m] ? kr : (pos[m] == kr ? p : pos[m]);
+      if (piv[m]) urc[m] = rc;  // 1/U_kk, kept for the diagonal-block inverse
+      alive[m] = alive[m] && !piv[m];
     }
 #pragma unroll
     for (int m = 0; m < MSE; ++m) {
-      const bool act = pos[m] > kr && pos[m] < R;
+      const bool act = alive[m];
       const double2 l = act ? cmul(pn[m][j], rc) : make_double2(0.0, 0.0);
       if (act) pn[m][j] = l;
 #pragma unroll
       for (int k = j + 1; k < 8; ++k)
         if (!(PODP_LL_ABLATE & 32) || k == j + 1) pn[m][k] = cfms(l, u[k], pn[m][k]);
     }
-    __syncwarp();  // sRow is rewritten by the next column
+    if constexpr (SROW) __syncwarp();  // sRow is rewritten by the next column
   }
+  __syncwarp();  // every lane has read its last pivot row before the strip is rewritten below
   // diagonal block L_cc \ U_cc -> strip c rows 0..7, with 1/U_kk stored in place of U_kk (the diagonal entries
   // are used only by the diagonal-block inverse D_c, which needs the reciprocals)
 #pragma unroll
@@ -534,14 +590,14 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
 template <int R, bool TM = false>
 __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, double om, const double2 *S,
                                        double2 *gY, double2 *gD, const double2 *gDiag, const int *sPerm, double *Pw,
-                                       int64_t t, int lane, uint32_t tm = 0) {
+                                       int64_t t, int lane, uint32_t tm = 0, const double2 *sB = nullptr) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
   double z[NT][2];
   {
-    const double2 *gb0 = reinterpret_cast<const double2 *>(op + a.L.b0);
-    const double2 *gb1 = reinterpret_cast<const double2 *>(op + a.L.b1);
+    const double2 *gb0 = sB ? sB : reinterpret_cast<const double2 *>(op + a.L.b0);
+    const double2 *gb1 = sB ? sB + 3 * R : reinterpret_cast<const double2 *>(op + a.L.b1);
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
       const int ph = sPerm[8 * tt + r4];
@@ -551,7 +607,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
         double v = 0.0;
         if (n < 6) {
           const int d = n < 3 ? n : n - 3;
-          const double2 x0 = __ldg(gb0 + d * R + ph), x1 = __ldg(gb1 + d * R + ph);
+          const double2 x0 = gb0[d * R + ph], x1 = gb1[d * R + ph];
           v = n < 3 ? fma(om, x1.x, x0.x) : fma(om, x1.y, x0.y);
         }
         z[tt][e] = v;
@@ -729,19 +785,27 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
         }
         if (info != 0) break;
       }
-      if (info == 0) lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm);
+      if (info == 0)
+        lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm,
+                            C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr);
     }
     lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
   };
 
-  auto stage_km = [&](int obj) {  // K and M of one object into shared memory (row stride R + 1), whole CTA
-    const double2 *k0p = reinterpret_cast<const double2 *>(a.ops + (size_t)obj * a.L.stride + a.L.K);
-    const double2 *m0p = reinterpret_cast<const double2 *>(a.ops + (size_t)obj * a.L.stride + a.L.M);
+  auto stage_km = [&](int obj) {  // K and M (row stride R + 1), b0 and b1 of one object -> shared memory, whole CTA
+    const double *o = a.ops + (size_t)obj * a.L.stride;
+    const double2 *k0p = reinterpret_cast<const double2 *>(o + a.L.K);
+    const double2 *m0p = reinterpret_cast<const double2 *>(o + a.L.M);
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
       const int i = e / R, j = e - i * R;
       sKM[i * (R + 1) + j] = __ldg(k0p + e);
       sKM[R * (R + 1) + i * (R + 1) + j] = __ldg(m0p + e);
+    }
+    double2 *sB = sKM + 2 * R * (R + 1);
+    for (int e = threadIdx.x; e < 3 * R; e += blockDim.x) {
+      sB[e] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b0) + e);
+      sB[3 * R + e] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b1) + e);
     }
   };
   if constexpr (SEG) {
