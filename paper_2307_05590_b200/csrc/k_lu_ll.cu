@@ -56,6 +56,9 @@ struct Cfg {
   // the remaining strips stay in shared memory after the virtual strip.  TM_COLS is chosen to maximise the warps per
   // SM under the shared-memory, register and tensor-memory limits (r = 48: all 15 tiles in 128 columns, 12 warps;
   // r = 80: 4 strips in 256 columns, 8 warps instead of 4; r = 96: 9 strips in 512 columns, 4 instead of 3)
+  // HYB_G (R >= 88): the strips that do not fit in tensor memory go to the warp's L2 scratch instead of shared
+  // memory, so that the warp count is set by tensor memory and registers (r = 96: 8 warps instead of 4)
+  static constexpr bool HYB_G = TM && R >= 88;
   static constexpr int tm_tiles(int tb) { return tb * (NT - 1) - tb * (tb - 1) / 2; }
   static constexpr int tm_fit(int cols) {
     int tb = 0;
@@ -66,7 +69,7 @@ struct Cfg {
   static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);  // register cap, see below
   static constexpr int tm_warps(int cols) {
     const int hyb = NT * (NT - 1) / 2 - tm_tiles(tm_fit(cols));
-    const int w_bytes = (NT + hyb) * 1024 + 9 * 16 + 2 * PERM_BYTES;
+    const int w_bytes = (NT + (HYB_G ? 0 : hyb)) * 1024 + 9 * 16 + 2 * PERM_BYTES;
     const int km = R <= 64 ? 2 * R * (R + 1) * 16 : 0;
     const int g_smem = (227 * 1024 - km) / w_bytes, g_tm = 4 * (512 / cols);
     const int g = g_smem < G_REG ? g_smem : G_REG;
@@ -82,7 +85,8 @@ struct Cfg {
   static constexpr int TM_TB = TM ? tm_fit(TM_COLS) : 0;
   static constexpr int TM_TILES = tm_tiles(TM_TB);       // M tiles per frequency in TMEM (8 columns each)
   static constexpr int HYB_TILES = NT * (NT - 1) / 2 - TM_TILES;
-  static constexpr int STRIP_TILES = TM ? NT + HYB_TILES : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
+  static constexpr int STRIP_TILES =
+      TM ? NT + (HYB_G ? 0 : HYB_TILES) : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
   static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16 * (TM ? 2 : 1);
   // KM (single-object launches, R <= 40, or with TM): K and M staged once per CTA in shared memory (row stride
@@ -102,7 +106,8 @@ struct Cfg {
   static constexpr int G_SR = G_SMEM < G_MAX ? G_SMEM : G_MAX;
   static constexpr int G = G_SR < G_TM ? G_SR : G_TM;    // warps (= concurrent frequencies) per CTA
   static_assert(!TM || TM_COLS * ((G + 3) / 4) <= 512, "M tiles do not fit in tensor memory");
-  static constexpr int GSCR_TILES = NT * (NT + 3) / 2;   // Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT
+  // per-warp L2 scratch: Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT (+ HYB_G: the hybrid strips)
+  static constexpr int GSCR_TILES = NT * (NT + 3) / 2 + (HYB_G ? HYB_TILES : 0);
   static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
   static_assert(TM || !DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
@@ -308,7 +313,7 @@ __device__ __forceinline__ double2 afrag_cstore_s(const double2 *g, int s, int l
 // an exactly zero pivot column at global step k.
 template <int R, int MSE, bool PIVOT, bool TM = false>
 __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPerm, double2 *gDiag, int lane,
-                                     uint32_t tm = 0, int *sMap = nullptr) {
+                                     uint32_t tm = 0, int *sMap = nullptr, double2 *Sh = nullptr) {
   constexpr int NT = R / 8;
   const int kb = 8 * c;
   double2 *St = TM ? S : S + strip_off<Cfg<8 * NT>::DIAG_L2>(NT, c) * 64;
@@ -465,8 +470,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
           tm_st8(tm + 8 * tm_tile(NT, c, t), row[q ^ swz(r4)], row[(4 + q) ^ swz(r4)]);
         }
       tm_wait_st();
-    } else {  // (R = 96) strips TB.. stay in shared memory, after the virtual strip
-      double2 *dst = S + strip_off_hyb(NT, TB, c) * 64;
+    } else {  // (R >= 72) strips TB.. stay in shared memory after the virtual strip (HYB_G: in the L2 scratch)
+      double2 *dst = Sh + strip_off_hyb(NT, TB, c) * 64;
       for (int e = 64 + lane; e < (NT - c) * 64; e += 32) dst[e] = St[e];
     }
     __syncwarp();
@@ -513,7 +518,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
       __syncwarp();
       for (int b = 0; b < c; ++b) {
         if (b >= TB) {
-          swap_rows_smem(S + strip_off_hyb(NT, TB, b) * 64 - 8 * 8 * b);
+          swap_rows_smem(Sh + strip_off_hyb(NT, TB, b) * 64 - 8 * 8 * b);
           continue;
         }
 #pragma unroll 1
@@ -558,7 +563,8 @@ namespace lull {
 template <int R, bool TM = false>
 __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], double (&ai)[R / 8][2], double2 *S,
                                             double2 *gY, const int *sPerm, const double2 *gK, const double2 *gM,
-                                            double s, int lane, int ldkm = R, uint32_t tm = 0) {
+                                            double s, int lane, int ldkm = R, uint32_t tm = 0,
+                                            const double2 *Sh = nullptr) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
@@ -573,7 +579,8 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
     ai[tt][1] = fma(s, m1.x, k1.y);
   }
   if constexpr (!(PODP_LL_ABLATE & 2))
-    for (int b = 0; b < c; ++b) body_dispatch<NT, TM>(b, ar, ai, S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
+    for (int b = 0; b < c; ++b)
+      body_dispatch<NT, TM>(b, ar, ai, TM ? Sh : S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
   double2 *St = TM ? S : S + strip_off<C::DIAG_L2>(NT, c) * 64;
 #pragma unroll
   for (int tt = 0; tt < NT; ++tt) {
@@ -590,7 +597,8 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
 template <int R, bool TM = false>
 __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, double om, const double2 *S,
                                        double2 *gY, double2 *gD, const double2 *gDiag, const int *sPerm, double *Pw,
-                                       int64_t t, int lane, uint32_t tm = 0, const double2 *sB = nullptr) {
+                                       int64_t t, int lane, uint32_t tm = 0, const double2 *sB = nullptr,
+                                       const double2 *Sh = nullptr) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
   const int r4 = lane >> 2, q = lane & 3;
@@ -616,7 +624,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   }
   if constexpr (!(PODP_LL_ABLATE & 8))
     [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
-      (body_rhs<NT, Bs, TM>(z, S, lane, tm), ...);
+      (body_rhs<NT, Bs, TM>(z, TM ? Sh : S, lane, tm), ...);
     }(std::make_integer_sequence<int, NT - 1>{});
   // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----------
   // DIAG_L2: the strips are no longer needed after the forward sweep, so the diagonal blocks are brought back from
@@ -739,6 +747,9 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
   double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
   double2 *gD = gY + (NT * (NT - 1) / 2) * 64;
   double2 *gDiag = gD + NT * 64;  // L\U diagonal blocks (panel order)
+  // TM: base of the strips kept outside tensor memory (tile offsets strip_off_hyb): shared memory after the virtual
+  // strip, or (HYB_G) the L2 scratch after the diagonal blocks
+  double2 *Sh = C::HYB_G ? gDiag + NT * 64 - NT * 64 : S;
 
   double2 *sKM = reinterpret_cast<double2 *>(smem_raw + (size_t)G * C::W_BYTES);
   // TM: 512 TMEM columns for the CTA (warp 0 allocates and frees); warp w uses the lanes of its SM sub-partition
@@ -773,21 +784,21 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
       __syncwarp();
       double ar[NT][2], ai[NT][2];
       for (int c = 0; c < NT; ++c) {
-        lull::column_tile<R, TM>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM, tm);
+        lull::column_tile<R, TM>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM, tm, Sh);
         __syncwarp();
         if constexpr (PODP_LL_ABLATE & 1) {
           info = 0;
         } else if constexpr (C::MS > 1) {
-          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap)
-                                  : lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap);
+          info = (R - 8 * c > 32) ? lull::panel<R, C::MS, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap, Sh)
+                                  : lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap, Sh);
         } else {
-          info = lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap);
+          info = lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap, Sh);
         }
         if (info != 0) break;
       }
       if (info == 0)
         lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm,
-                            C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr);
+                            C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr, Sh);
     }
     lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
@@ -894,24 +905,30 @@ static cudaError_t launch_t(const EvalArgs &a, cudaStream_t s, int sms) {
 }
 }  // namespace lull
 
+namespace lull {
+template <int R>
+constexpr size_t scratch_tiles() {  // per SM: the largest G x GSCR_TILES over the variants launch_t may pick
+  constexpr size_t p = (size_t)Cfg<R>::G * Cfg<R>::GSCR_TILES, k = (size_t)Cfg<R, true>::G * Cfg<R, true>::GSCR_TILES;
+  if constexpr (R % 8 == 0 && R >= 40) {
+    constexpr size_t t = (size_t)Cfg<R, false, true>::G * Cfg<R, false, true>::GSCR_TILES;
+    return (p > k ? p : k) > t ? (p > k ? p : k) : t;
+  } else {
+    return p > k ? p : k;
+  }
+}
+}  // namespace lull
+
 size_t lu_ll_scratch_bytes(int R, int sms) {
-  if (R % 8 || R > 96) return 0;
-  const int NT = R / 8;
-  int G = 0;
+  size_t tiles = 0;
   switch (R) {
-#define PODP_CASE(RR)                                                                              \
-  case RR:                                                                                         \
-    G = lull::Cfg<RR>::G > lull::Cfg<RR, false, true>::G ? lull::Cfg<RR>::G : lull::Cfg<RR, false, true>::G; \
-    break;
-    PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64) PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
-#undef PODP_CASE
 #define PODP_CASE(RR) \
-  case RR: G = lull::Cfg<RR>::G; break;
-    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32)
+  case RR: tiles = lull::scratch_tiles<RR>(); break;
+    PODP_CASE(8) PODP_CASE(16) PODP_CASE(24) PODP_CASE(32) PODP_CASE(40) PODP_CASE(48) PODP_CASE(56) PODP_CASE(64)
+    PODP_CASE(72) PODP_CASE(80) PODP_CASE(88) PODP_CASE(96)
 #undef PODP_CASE
     default: return 0;
   }
-  return (size_t)sms * G * (NT * (NT + 3) / 2) * 1024;
+  return (size_t)sms * tiles * 1024;
 }
 
 cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
