@@ -34,6 +34,10 @@
 #ifndef PODP_LL_ABLATE
 #define PODP_LL_ABLATE 0
 #endif
+// Dev: PODP_LL_SYNC = 0 / 1 forces the per-frequency CTA rendezvous (Cfg::LOCKSTEP) off / on for every size.
+#ifndef PODP_LL_SROW_MAX
+#define PODP_LL_SROW_MAX 40
+#endif
 
 namespace podp {
 
@@ -66,7 +70,10 @@ struct Cfg {
     return tb;
   }
   static constexpr int PERM_BYTES = ((R * 4 + 15) / 16) * 16;
-  static constexpr int G_REG = R <= 32 ? 16 : (R <= 48 ? 12 : 8);  // register cap, see below
+  #ifndef PODP_LL_GREG48
+#define PODP_LL_GREG48 12
+#endif
+  static constexpr int G_REG = R <= 32 ? 16 : (R <= 40 ? 12 : (R <= 48 ? PODP_LL_GREG48 : 8));  // register cap, see below
   static constexpr int tm_warps(int cols) {
     const int hyb = NT * (NT - 1) / 2 - tm_tiles(tm_fit(cols));
     const int w_bytes = (NT + (HYB_G ? 0 : hyb)) * 1024 + 9 * 16 + 2 * PERM_BYTES;
@@ -93,7 +100,7 @@ struct Cfg {
   // R + 1 complex), so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 ->
   // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
   // (+ b0 and b1, 3R complex each, read by the right-hand-side assembly of every frequency)
-  static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? (2 * R * (R + 1) + 6 * R) * 16 : 0;
+  static constexpr int KM_BYTES = (KM || TM) && R <= 64 ? (2 * R * (R + 1) + 6 * (R + 2)) * 16 : 0;
   static constexpr int G_SMEM = (227 * 1024 - KM_BYTES) / W_BYTES;
   // warp cap G_REG (measured: ptxas allocates <= 168 registers up to R = 48, i.e. 3 warps per SM sub-partition,
   // 224-255 above, i.e. 2; at R <= 32 16 warps with 128 registers are fastest)
@@ -107,10 +114,22 @@ struct Cfg {
   static constexpr int G = G_SR < G_TM ? G_SR : G_TM;    // warps (= concurrent frequencies) per CTA
   static_assert(!TM || TM_COLS * ((G + 3) / 4) <= 512, "M tiles do not fit in tensor memory");
   // per-warp L2 scratch: Y_{t,c} (t < c): NT(NT-1)/2, D_t: NT, L\U diag: NT (+ HYB_G: the hybrid strips)
+  // LOCKSTEP: the warps of a CTA start every frequency together (one __syncthreads per frequency).  The kernel is
+  // ~150 KB of straight-line code that each warp streams once per frequency; 12 warps at 12 different places miss the
+  // SM's instruction cache (ncu at r = 48: icc hit rate 86 %, GPC-level instruction requests at 67 % of peak,
+  // no_instruction 0.72 stall cycles per issue); in step they share each fetched line (hit rate 96 %, requests 26 %):
+  // r = 48 solve 3.13 -> 2.84 ms per 1e5.  Measured slower where the code is smaller or fewer warps run (R <= 40:
+  // 0.5-8 %; R >= 56: 0-1.5 %), so only the R = 48 tensor-memory variant takes it.
+#ifdef PODP_LL_SYNC
+  static constexpr bool LOCKSTEP = PODP_LL_SYNC != 0;
+#else
+  static constexpr bool LOCKSTEP = TM && R == 48;
+#endif
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2 + (HYB_G ? HYB_TILES : 0);
   static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
-  static_assert(TM || !DIAG_L2 || 2 * NT <= STRIP_TILES, "diagonal blocks and D_t must fit in the strip area");
+  static_assert(TM || !DIAG_L2 || 2 * NT * 65 <= STRIP_TILES * 64 + 9,
+                "diagonal blocks and D_t (stride 65) must fit in the strip area");
 };
 
 // Shared-memory tile offset of the "virtual strip" of panel b: its diagonal-block tile followed by its M tiles
@@ -128,9 +147,10 @@ template <bool DIAG_L2>
 __host__ __device__ constexpr int strip_off(int NT, int b) {
   return DIAG_L2 ? (NT - 2 - b) * (NT - 1 - b) / 2 : b * NT - b * (b - 1) / 2;
 }
-// row swizzle: slot = k ^ swz(i & 7) makes both lane = row reads (8 rows, same k) and A-fragment reads (rows 2j,
-// 2j+1 x 4 consecutive k) hit 8 distinct 16-byte bank groups
-__device__ __forceinline__ int swz(int i) { return ((i & 1) << 2) | ((i >> 1) & 3); }
+// row swizzle: slot = k ^ swz(i & 7) makes lane = row accesses (8 rows, same k), A-fragment reads (rows 2j, 2j+1 x
+// 4 consecutive k: the two rows' swizzles differ in bit 2) and C-fragment stores (rows 2j, 2j+1 x even or odd k: they
+// differ in bit 0) each hit 8 distinct 16-byte bank groups
+__device__ __forceinline__ int swz(int i) { return ((i & 1) * 5) ^ ((i >> 1) & 3); }
 
 __device__ __forceinline__ double selp_f64(double a, double b, int p) {  // p ? a : b
   double r;
@@ -302,10 +322,11 @@ __device__ __forceinline__ double2 afrag_cstore(const double2 *g, int s, int lan
   const int k = 4 * s + (lane & 3);
   return __ldcg(g + 2 * (4 * (lane >> 2) + (k >> 1)) + (k & 1));
 }
-// the same from shared memory
+// the same from shared memory, rows XOR-swizzled (element (i, k) at 8 i + (k ^ 4 (i & 1))): rows 2j and 2j+1 of a
+// quarter warp fall into different halves of the 128-byte line pair (conflict-free)
 __device__ __forceinline__ double2 afrag_cstore_s(const double2 *g, int s, int lane) {
-  const int k = 4 * s + (lane & 3);
-  return g[2 * (4 * (lane >> 2) + (k >> 1)) + (k & 1)];
+  const int k = 4 * s + (lane & 3), i = lane >> 2;
+  return g[8 * i + (k ^ ((i & 1) << 2))];
 }
 
 // Unblocked LU with partial pivoting of panel c (rows 8c .. R-1 of strip c, lane = row), M_tc = L_tc L_cc^{-1},
@@ -338,7 +359,7 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
   // (ties: lowest slot).  R <= 40 (SROW): the pivot row's owner copies it to the 9-entry sRow and the key carries
   // the position (ties: lowest position) -- fewer shared-memory wavefronts, measured faster where 16 warps share
   // them (r = 24 .. 40: 1.5-3 %; R >= 48 the other way round, r = 64: 3 %).
-  constexpr bool SROW = R <= 40;
+  constexpr bool SROW = R <= PODP_LL_SROW_MAX;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int kr = kb + j;
@@ -458,8 +479,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
     // diagonal block -> L2 scratch; the panel's M tiles (rows of tiles c+1..NT-1) -> tensor memory in A-fragment
     // order (lane (r4, q) keeps M[r4][q] and M[r4][q + 4] of each tile); the shared-memory strip is then free
     __syncwarp();
-    gDiag[c * 64 + 2 * lane] = St[2 * lane];
-    gDiag[c * 64 + 2 * lane + 1] = St[2 * lane + 1];
+    gDiag[c * 64 + lane] = St[lane];
+    gDiag[c * 64 + 32 + lane] = St[32 + lane];
     const int r4 = lane >> 2, q = lane & 3;
     constexpr int TB = Cfg<R, false, TM>::TM_TB;
     if (c < TB) {
@@ -547,8 +568,8 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
   if constexpr (Cfg<R>::DIAG_L2 && !TM) {
     // the diagonal block (L_cc \ U_cc with 1/U_kk on the diagonal, swizzled rows) -> L2 scratch for the inverses;
     // its shared-memory tile is reused by the next strip
-    gDiag[c * 64 + 2 * lane] = St[2 * lane];
-    gDiag[c * 64 + 2 * lane + 1] = St[2 * lane + 1];
+    gDiag[c * 64 + lane] = St[lane];
+    gDiag[c * 64 + 32 + lane] = St[32 + lane];
     __syncwarp();
   }
   return 0;
@@ -604,8 +625,10 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   const int r4 = lane >> 2, q = lane & 3;
   double z[NT][2];
   {
+    // shared-memory copy: rows padded to R + 2 entries (the three directions fall into different banks)
+    const int ldb = sB ? R + 2 : R;
     const double2 *gb0 = sB ? sB : reinterpret_cast<const double2 *>(op + a.L.b0);
-    const double2 *gb1 = sB ? sB + 3 * R : reinterpret_cast<const double2 *>(op + a.L.b1);
+    const double2 *gb1 = sB ? sB + 3 * (R + 2) : reinterpret_cast<const double2 *>(op + a.L.b1);
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
       const int ph = sPerm[8 * tt + r4];
@@ -615,7 +638,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
         double v = 0.0;
         if (n < 6) {
           const int d = n < 3 ? n : n - 3;
-          const double2 x0 = gb0[d * R + ph], x1 = gb1[d * R + ph];
+          const double2 x0 = gb0[d * ldb + ph], x1 = gb1[d * ldb + ph];
           v = n < 3 ? fma(om, x1.x, x0.x) : fma(om, x1.y, x0.y);
         }
         z[tt][e] = v;
@@ -631,11 +654,15 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   // the L2 scratch into shared-memory tiles 0..NT-1 (one round of independent loads) and D_t goes to tiles
   // NT..2NT-1, where the back substitution reads it (no L2 round trips on either chain)
   // (TM: the shared-memory strip has only NT tiles; D_t overwrites the staged blocks in place, see below)
-  double2 *sD = const_cast<double2 *>(S) + (TM ? 0 : NT * 64);
+  // staged blocks and D_t sit at a stride of DS = 65 entries (the 4 blocks a pass works on then fall into different
+  // 16-byte bank groups: their broadcast reads cost 1 wavefront instead of 4); the spill-over lands in sRow
+  constexpr int DS = (TM && NT > 9) ? 64 : 65;
+  static_assert(!TM || NT * DS <= NT * 64 + 9, "staged diagonal blocks overrun sRow");
+  double2 *sD = const_cast<double2 *>(S) + (TM ? 0 : NT * DS);
   if constexpr (C::DIAG_L2 || TM) {
     __syncwarp();
     double2 *Sw = const_cast<double2 *>(S);
-    for (int e = lane; e < NT * 64; e += 32) Sw[e] = __ldcg(gDiag + e);
+    for (int e = lane; e < NT * 64; e += 32) Sw[(e >> 6) * DS + (e & 63)] = __ldcg(gDiag + e);
     __syncwarp();
   }
   if constexpr (!(PODP_LL_ABLATE & 4)) {
@@ -647,7 +674,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
       const int tdc = act ? td : NT - 1;  // idle lanes recompute the last block (results discarded)
       {
         // L\U diagonal block of panel td: staged copy (DIAG_L2, TM) or rows 0..7 of strip td
-        const double2 *Dg = (C::DIAG_L2 || TM) ? S + tdc * 64 : S + strip_off<false>(NT, tdc) * 64;
+        const double2 *Dg = (C::DIAG_L2 || TM) ? S + tdc * DS : S + strip_off<false>(NT, tdc) * 64;
         double2 y[8], x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -663,11 +690,14 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
           for (int k = i + 1; k < 8; ++k) acc = cfms(Dg[i * 8 + (k ^ swz(i))], x[k], acc);
           x[i] = cmul(acc, Dg[i * 8 + (i ^ swz(i))]);  // 1/U_ii (stored by the panel)
         }
-        double2 *dt = (C::DIAG_L2 || TM) ? sD + tdc * 64 : gD + tdc * 64;
+        double2 *dt = (C::DIAG_L2 || TM) ? sD + tdc * DS : gD + tdc * 64;
         if constexpr (TM) __syncwarp();  // D_t overwrites the staged block it was computed from
         if (act) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+          for (int i = 0; i < 8; ++i) {
+            if constexpr (C::DIAG_L2 || TM) dt[8 * i + (j ^ ((i & 1) << 2))] = x[i];  // see afrag_cstore_s
+            else dt[2 * (4 * i + (j >> 1)) + (j & 1)] = x[i];
+          }
         }
       }
     }
@@ -678,8 +708,8 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   for (int tt = NT - 1; tt >= 0; --tt) {
     double b1[2], b2[2];
     rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
-    const double2 d0 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * 64, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
-    const double2 d1 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * 64, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
+    const double2 d0 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * DS, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
+    const double2 d1 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * DS, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
     double x0 = 0.0, x1 = 0.0;
     dmma(x0, x1, d0.x, b1[0]);
     dmma(x0, x1, d0.y, b2[0]);
@@ -770,20 +800,25 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
   }
 
   // one evaluation t = (obj, f) by this warp
-  auto process = [&](int64_t t, int obj, int64_t f) {
+  // CTA-wide rendezvous of the warps before each frequency (Cfg::LOCKSTEP); every warp of the CTA executes it the
+  // same number of times (the evaluation loops below are CTA-uniform, a warp without work passes valid = false)
+  auto rendezvous = [&]() {
+    if constexpr (C::LOCKSTEP) __syncthreads();
+  };
+  auto process = [&](int64_t t, int obj, int64_t f, bool valid) {
     const double *op = a.ops + (size_t)obj * a.L.stride;
-    const double om = a.omega[f];
+    const double om = valid ? a.omega[f] : 0.0;
     const double s = om * op[a.L.scal + SC_NU];
     const double2 *gK = C::KM_BYTES ? sKM : reinterpret_cast<const double2 *>(op + a.L.K);
     const double2 *gM = C::KM_BYTES ? sKM + R * (R + 1) : reinterpret_cast<const double2 *>(op + a.L.M);
     constexpr int LDKM = C::KM_BYTES ? R + 1 : R;
     double *Pw = reinterpret_cast<double *>(a.Pws + (size_t)t * 3 * R);
-    int info = isfinite(om) ? 0 : -1;
-    if (info == 0) {
-      for (int i = lane; i < R; i += 32) sPerm[i] = i;
-      __syncwarp();
-      double ar[NT][2], ai[NT][2];
-      for (int c = 0; c < NT; ++c) {
+    int info = valid ? (isfinite(om) ? 0 : -1) : -2;
+    for (int i = lane; i < R; i += 32) sPerm[i] = i;
+    __syncwarp();
+    double ar[NT][2], ai[NT][2];
+    for (int c = 0; c < NT; ++c) {
+      if (info == 0) {
         lull::column_tile<R, TM>(c, ar, ai, S, gY, sPerm, gK, gM, s, lane, LDKM, tm, Sh);
         __syncwarp();
         if constexpr (PODP_LL_ABLATE & 1) {
@@ -794,13 +829,12 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
         } else {
           info = lull::panel<R, 1, PIVOT, TM>(c, S, sRow, sPerm, gDiag, lane, tm, sMap, Sh);
         }
-        if (info != 0) break;
       }
-      if (info == 0)
-        lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm,
-                            C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr, Sh);
     }
-    lull::fail_out(a, Pw, R, t, info, lane);
+    if (info == 0)
+      lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm,
+                          C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr, Sh);
+    if (valid) lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
   };
 
@@ -815,8 +849,9 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
     }
     double2 *sB = sKM + 2 * R * (R + 1);
     for (int e = threadIdx.x; e < 3 * R; e += blockDim.x) {
-      sB[e] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b0) + e);
-      sB[3 * R + e] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b1) + e);
+      const int d = e / R, i = e - d * R;
+      sB[d * (R + 2) + i] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b0) + e);
+      sB[3 * (R + 2) + d * (R + 2) + i] = __ldg(reinterpret_cast<const double2 *>(o + a.L.b1) + e);
     }
   };
   if constexpr (SEG) {
@@ -832,7 +867,10 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
       stage_km(obj);
       __syncthreads();
       const int64_t fbase = (int64_t)obj * a.F;
-      for (int64_t t = seg + wid; t < seg_end; t += G) process(t, obj, t - fbase);
+      for (int64_t t = seg + wid; t - wid < seg_end; t += G) {
+        rendezvous();
+        process(t, obj, t - fbase, t < seg_end);
+      }
       seg = seg_end;
       ++obj;
     }
@@ -850,8 +888,9 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
       f -= a.F;
       ++obj;
     }
-    for (int64_t t = gw; t < total; t += nw) {
-      process(t, obj, f);
+    for (int64_t t = gw; t - wid < total; t += nw) {
+      rendezvous();
+      process(t, obj, f, t < total);
       f += nw;
       while (f >= a.F) {
         f -= a.F;
@@ -934,6 +973,9 @@ size_t lu_ll_scratch_bytes(int R, int sms) {
 cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
   if (!a.gscr) return cudaErrorInvalidValue;
   switch (a.L.R) {
+#ifdef PODP_LL_ONLY_R  // dev: instantiate one size only (fast ptxas iterations)
+    case PODP_LL_ONLY_R: return lull::launch_t<PODP_LL_ONLY_R>(a, s, sms);
+#else
     case 8: return lull::launch_t<8>(a, s, sms);
     case 16: return lull::launch_t<16>(a, s, sms);
     case 24: return lull::launch_t<24>(a, s, sms);
@@ -946,6 +988,7 @@ cudaError_t launch_lu_ll(const EvalArgs &a, cudaStream_t s, int sms) {
     case 80: return lull::launch_t<80>(a, s, sms);
     case 88: return lull::launch_t<88>(a, s, sms);
     case 96: return lull::launch_t<96>(a, s, sms);
+#endif
     default: return cudaErrorNotSupported;
   }
 }
