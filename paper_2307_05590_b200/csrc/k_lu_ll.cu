@@ -120,6 +120,14 @@ struct Cfg {
   // no_instruction 0.72 stall cycles per issue); in step they share each fetched line (hit rate 96 %, requests 26 %):
   // r = 48 solve 3.13 -> 2.84 ms per 1e5.  Measured slower where the code is smaller or fewer warps run (R <= 40:
   // 0.5-8 %; R >= 56: 0-1.5 %), so only the R = 48 tensor-memory variant takes it.
+  // GAUSS3: three-product complex tile multiplication in the left-looking updates (see body): 330 instead of 440
+  // DMMA per frequency at r = 48.  Measured per 1e5: r = 40 2.07 -> 1.95 ms, r = 48 2.76 -> 2.68, r = 64 5.45 -> 5.38,
+  // r = 32 1.18 -> 1.17; not faster at r <= 24 (few updates) and slower at r = 96 (20.1 vs 19.7: registers)
+#ifdef PODP_LL_GAUSS3
+  static constexpr bool GAUSS3 = PODP_LL_GAUSS3 != 0;
+#else
+  static constexpr bool GAUSS3 = R >= 32 && R <= 64;
+#endif
 #ifdef PODP_LL_SYNC
   static constexpr bool LOCKSTEP = PODP_LL_SYNC != 0;
 #else
@@ -213,18 +221,30 @@ __device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double
 
 // Column c, block b: Y_{b,c} = acc_b is final -> scratch (C-fragment order) and acc_t -= M_{t,b} Y_{b,c}, t > b.
 // The M tiles come from shared memory, or (TM) from tensor memory: one tcgen05.ld per tile, one wait for all.
-template <int NT, int B, bool TM = false>
-__device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S, double2 *gY,
-                                     int lane, uint32_t tm = 0) {
+// M3 (Gauss's three-product complex multiplication): with Ms = Mr + Mi, the three running sums
+//   ak -= Ms Yr,  ar += Mi (Yr + Yi),  ai += Mr (Yr - Yi)   give   Re = ar + ak,  Im = ai + ak
+// (Re(MY) = Ms Yr - Mi (Yr + Yi), Im(MY) = Ms Yr + Mr (Yi - Yr)): 6 DMMA per complex tile product instead of 8, for
+// one more accumulator set per column tile and 2 additions per M tile; ar/ai of tile B are final only as ar + ak,
+// ai + ak (formed here for Y_{B,c}, and by column_tile for the rows that go to the panel).
+template <int NT, int B, bool TM = false, bool M3 = false>
+__device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], double (&ak)[NT][2], const double2 *S,
+                                     double2 *gY, int lane, uint32_t tm = 0) {
+  if constexpr (M3) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      ar[B][e] += ak[B][e];
+      ai[B][e] += ak[B][e];
+    }
+  }
   gY[2 * lane] = make_double2(ar[B][0], ai[B][0]);
   gY[2 * lane + 1] = make_double2(ar[B][1], ai[B][1]);
-  double nyr[2], yi[2], nyi[2];
+  double nyr[2], yi[2], nyi[2];  // M3: -Yr, Yr + Yi, Yr - Yi
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const double r = frag_c2b(ar[B][0], ar[B][1], s, lane), i = frag_c2b(ai[B][0], ai[B][1], s, lane);
     nyr[s] = -r;
-    yi[s] = i;
-    nyi[s] = -i;
+    yi[s] = M3 ? r + i : i;
+    nyi[s] = M3 ? r - i : -i;
   }
   const int r4 = lane >> 2, q = lane & 3;
   constexpr int TB = Cfg<8 * NT, false, TM>::TM_TB;
@@ -252,24 +272,34 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], c
       m0 = row[k0];
       m1 = row[k1];
     }
-    // acc -= M Y :  Re += Mr (-Yr) + Mi Yi ;  Im += Mr (-Yi) + Mi (-Yr)
-    dmma(ar[t][0], ar[t][1], m0.x, nyr[0]);
-    dmma(ai[t][0], ai[t][1], m0.x, nyi[0]);
-    dmma(ar[t][0], ar[t][1], m0.y, yi[0]);
-    dmma(ai[t][0], ai[t][1], m0.y, nyr[0]);
-    dmma(ar[t][0], ar[t][1], m1.x, nyr[1]);
-    dmma(ai[t][0], ai[t][1], m1.x, nyi[1]);
-    dmma(ar[t][0], ar[t][1], m1.y, yi[1]);
-    dmma(ai[t][0], ai[t][1], m1.y, nyr[1]);
+    if constexpr (M3) {
+      const double s0 = m0.x + m0.y, s1 = m1.x + m1.y;
+      dmma(ak[t][0], ak[t][1], s0, nyr[0]);
+      dmma(ar[t][0], ar[t][1], m0.y, yi[0]);
+      dmma(ai[t][0], ai[t][1], m0.x, nyi[0]);
+      dmma(ak[t][0], ak[t][1], s1, nyr[1]);
+      dmma(ar[t][0], ar[t][1], m1.y, yi[1]);
+      dmma(ai[t][0], ai[t][1], m1.x, nyi[1]);
+    } else {
+      // acc -= M Y :  Re += Mr (-Yr) + Mi Yi ;  Im += Mr (-Yi) + Mi (-Yr)
+      dmma(ar[t][0], ar[t][1], m0.x, nyr[0]);
+      dmma(ai[t][0], ai[t][1], m0.x, nyi[0]);
+      dmma(ar[t][0], ar[t][1], m0.y, yi[0]);
+      dmma(ai[t][0], ai[t][1], m0.y, nyr[0]);
+      dmma(ar[t][0], ar[t][1], m1.x, nyr[1]);
+      dmma(ai[t][0], ai[t][1], m1.x, nyi[1]);
+      dmma(ar[t][0], ar[t][1], m1.y, yi[1]);
+      dmma(ai[t][0], ai[t][1], m1.y, nyr[1]);
+    }
   }
 }
 
-template <int NT, bool TM = false, int B = 0>
-__device__ __forceinline__ void body_dispatch(int b, double (&ar)[NT][2], double (&ai)[NT][2], const double2 *S,
-                                              double2 *gY, int lane, uint32_t tm = 0) {
+template <int NT, bool TM = false, bool M3 = false, int B = 0>
+__device__ __forceinline__ void body_dispatch(int b, double (&ar)[NT][2], double (&ai)[NT][2], double (&ak)[NT][2],
+                                              const double2 *S, double2 *gY, int lane, uint32_t tm = 0) {
   if constexpr (B < NT - 1) {
-    if (b == B) body<NT, B, TM>(ar, ai, S, gY, lane, tm);
-    else body_dispatch<NT, TM, B + 1>(b, ar, ai, S, gY, lane, tm);
+    if (b == B) body<NT, B, TM, M3>(ar, ai, ak, S, gY, lane, tm);
+    else body_dispatch<NT, TM, M3, B + 1>(b, ar, ai, ak, S, gY, lane, tm);
   }
 }
 
@@ -599,13 +629,26 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
     ar[tt][1] = fma(-s, m1.y, k1.x);
     ai[tt][1] = fma(s, m1.x, k1.y);
   }
+  constexpr bool M3 = Cfg<R, false, TM>::GAUSS3;
+  double ak[NT][2];
+  if constexpr (M3) {
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) ak[tt][0] = ak[tt][1] = 0.0;
+  }
   if constexpr (!(PODP_LL_ABLATE & 2))
     for (int b = 0; b < c; ++b)
-      body_dispatch<NT, TM>(b, ar, ai, TM ? Sh : S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
+      body_dispatch<NT, TM, M3>(b, ar, ai, ak, TM ? Sh : S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
   double2 *St = TM ? S : S + strip_off<C::DIAG_L2>(NT, c) * 64;
 #pragma unroll
   for (int tt = 0; tt < NT; ++tt) {
     if (tt >= c) {
+      if constexpr (M3) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          ar[tt][e] += ak[tt][e];
+          ai[tt][e] += ak[tt][e];
+        }
+      }
       double2 *row = St + (8 * (tt - c) + r4) * 8;
       row[(2 * q) ^ swz(r4)] = make_double2(ar[tt][0], ai[tt][0]);
       row[(2 * q + 1) ^ swz(r4)] = make_double2(ar[tt][1], ai[tt][1]);
@@ -803,8 +846,18 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
   // CTA-wide rendezvous of the warps before each frequency (Cfg::LOCKSTEP); every warp of the CTA executes it the
   // same number of times (the evaluation loops below are CTA-uniform, a warp without work passes valid = false)
   auto rendezvous = [&]() {
+#ifdef PODP_LL_GROUP  // dev: rendezvous within groups of PODP_LL_GROUP warps only
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + wid / PODP_LL_GROUP), "r"(32 * PODP_LL_GROUP) : "memory");
+#else
     if constexpr (C::LOCKSTEP) __syncthreads();
+#endif
   };
+#ifdef PODP_LL_STAGGER  // dev: group g starts g * PODP_LL_STAGGER cycles late
+  {
+    const long long t0 = clock64(), wait = (long long)(wid / PODP_LL_GROUP) * PODP_LL_STAGGER;
+    while (clock64() - t0 < wait) __nanosleep(200);
+  }
+#endif
   auto process = [&](int64_t t, int obj, int64_t f, bool valid) {
     const double *op = a.ops + (size_t)obj * a.L.stride;
     const double om = valid ? a.omega[f] : 0.0;
