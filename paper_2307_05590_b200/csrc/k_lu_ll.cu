@@ -133,6 +133,14 @@ struct Cfg {
 #else
   static constexpr bool LOCKSTEP = TM && R == 48;
 #endif
+  // the rendezvous is taken every LOCKSTEP_EVERY-th frequency (power of two): the warps drift apart slowly, and a
+  // barrier per frequency costs its wait for the slowest warp (r = 48: every 1 / 4 / 16 / 64: 2.65 / 2.60 / 2.58 /
+  // 2.59 ms per 1e5)
+#ifdef PODP_LL_SYNC_EVERY
+  static constexpr int LOCKSTEP_EVERY = PODP_LL_SYNC_EVERY;
+#else
+  static constexpr int LOCKSTEP_EVERY = 16;
+#endif
   static constexpr int GSCR_TILES = NT * (NT + 3) / 2 + (HYB_G ? HYB_TILES : 0);
   static constexpr size_t BYTES = (size_t)G * W_BYTES + KM_BYTES;
   static_assert(G >= 1, "strips do not fit in shared memory");
@@ -481,9 +489,11 @@ __device__ __forceinline__ int panel(int c, double2 *S, double2 *sRow, int *sPer
 #pragma unroll
   for (int m = 0; m < MSE; ++m)
     if (pos[m] >= kb && pos[m] < kb + 8) {
+      double2 *rowp = St + (pos[m] - kb) * 8;
+      const int sw = swz(pos[m] & 7);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        St[(pos[m] - kb) * 8 + (k ^ swz(pos[m] & 7))] = (k == pos[m] - kb) ? urc[m] : pn[m][k];
+      for (int k = 0; k < 8; ++k) rowp[k ^ sw] = pn[m][k];
+      rowp[(pos[m] - kb) ^ sw] = urc[m];  // same lane, program order: the reciprocal replaces U_kk
     }
   __syncwarp();
   // rows below: m L_cc = l  (k = 7 .. 0: m_k = l_k - sum_{jj > k} m_jj L_cc[jj][k]), then store M rows
@@ -920,8 +930,9 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
       stage_km(obj);
       __syncthreads();
       const int64_t fbase = (int64_t)obj * a.F;
+      int it = 0;
       for (int64_t t = seg + wid; t - wid < seg_end; t += G) {
-        rendezvous();
+        if ((it++ & (C::LOCKSTEP_EVERY - 1)) == 0) rendezvous();
         process(t, obj, t - fbase, t < seg_end);
       }
       seg = seg_end;
@@ -935,14 +946,14 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
       stage_km(0);
       __syncthreads();
     }
-    int obj = 0;
+    int obj = 0, it = 0;
     int64_t f = gw;
     while (f >= a.F) {
       f -= a.F;
       ++obj;
     }
     for (int64_t t = gw; t - wid < total; t += nw) {
-      rendezvous();
+      if ((it++ & (C::LOCKSTEP_EVERY - 1)) == 0) rendezvous();
       process(t, obj, f, t < total);
       f += nw;
       while (f >= a.F) {
