@@ -74,7 +74,12 @@ enum {
      solution panel with bulk-copy (TMA) staging (k_mpt_gemm.cu) instead of the default operator-stationary kernel;
      one object, padded r in {24, 48, 96}, not with PODP_FLAG_PENCIL (else PODP_ERR_UNSUPPORTED).  Same results up
      to rounding. */
-  PODP_FLAG_MPT_GEMM = 1u << 13
+  PODP_FLAG_MPT_GEMM = 1u << 13,
+  /* Measurement only (A/B): the contraction kernel with two frequencies per lane (halves the shared-memory operator
+     traffic, + 13 % executed flops; measured slower: 1.00 vs 0.94 ms per 1e5 at r = 48); one object, padded r = 48,
+     not with PODP_FLAG_PENCIL, PODP_FLAG_MPT_GEMM or the per-direction form (else PODP_ERR_UNSUPPORTED; the
+     per-direction form ignores it).  Same results up to rounding. */
+  PODP_FLAG_MPT_PAIR = 1u << 14
 };
 
 /* Operators of ONE object (host pointers; copied, validated and packed by podp_create; caller keeps ownership).

@@ -679,7 +679,8 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
   if (!omega_d || !T1_d || !I_d || !Delta_d) return fail(PODP_ERR_ARG, "null omega/output pointer");
   if ((flags & PODP_FLAG_OUT_P) && !P_d) return fail(PODP_ERR_ARG, "PODP_FLAG_OUT_P set but P_d is NULL");
   const int known = PODP_FLAG_OUT_R | PODP_FLAG_OUT_P | PODP_FLAG_NO_PIVOT | PODP_FLAG_PENCIL | PODP_FLAG_LU_LL |
-                    PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC | PODP_FLAG_MPT_GEMM;
+                    PODP_FLAG_LU_BLK | PODP_FLAG_LU_DYN | PODP_FLAG_LU_GENERIC | PODP_FLAG_MPT_GEMM |
+                    PODP_FLAG_MPT_PAIR;
   if (flags & ~known) return fail(PODP_ERR_ARG, "unknown flag bits 0x%x", flags & ~known);
   DeviceGuard guard(c->device);
   if (!guard.ok) return fail(PODP_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
@@ -689,6 +690,8 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
   SolverKind ker;
   podp_status st0 = pick_solver(R, flags, &ker);
   if (st0 != PODP_OK) return st0;
+  if ((flags & PODP_FLAG_MPT_PAIR) && (c->n_obj != 1 || (flags & (PODP_FLAG_PENCIL | PODP_FLAG_MPT_GEMM)) || R != 48))
+    return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_MPT_PAIR: one object, padded r = 48, no pencil");
   if ((flags & PODP_FLAG_MPT_GEMM) && (c->n_obj != 1 || (flags & PODP_FLAG_PENCIL) || !(R == 24 || R == 48 || R == 96)))
     return fail(PODP_ERR_UNSUPPORTED, "PODP_FLAG_MPT_GEMM: one object, padded r in {24, 48, 96}, no pencil");
   if (flags & PODP_FLAG_PENCIL) {

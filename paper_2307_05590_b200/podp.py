@@ -26,6 +26,7 @@ FLAG_LU_BLK = 1 << 9
 FLAG_LU_DYN = 1 << 10
 FLAG_LU_GENERIC = 1 << 11
 FLAG_MPT_GEMM = 1 << 13
+FLAG_MPT_PAIR = 1 << 14
 R_MAX = 128
 STATUS_NAMES = {0: "PODP_OK", 1: "PODP_ERR_ARG", 2: "PODP_ERR_CUDA", 3: "PODP_ERR_OOM", 4: "PODP_ERR_UNSUPPORTED",
                 5: "PODP_ERR_NONFINITE", 6: "PODP_ERR_NOT_HERMITIAN", 7: "PODP_ERR_NO_CANDIDATES"}

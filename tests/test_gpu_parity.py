@@ -577,3 +577,23 @@ def test_mpt_gemm_variant_parity(torch_cuda, r, F):
     res = run_gpu(torch, ops, omega, flags=FLAG_OUT_R | FLAG_MPT_GEMM)
     assert (res["info"] == 0).all()
     check_parity(ops, omega, res)
+
+
+@pytest.mark.parametrize("r,F", [(48, 257), (48, 5), (47, 131), (41, 64)])
+def test_mpt_paired_and_single_kernels_parity(torch_cuda, r, F):
+    """The default contraction kernel and the A/B kernel with two frequencies per lane (PODP_FLAG_MPT_PAIR, padded
+    r = 48) both match the oracle per entry, including ragged last tiles (F not a multiple of 32, odd F: the second
+    frequency of a lane pair is missing) and padded r."""
+    torch = torch_cuda
+    from paper_2307_05590_b200 import FLAG_MPT_PAIR, FLAG_OUT_R
+    ops = g.make_operators(r if r % 2 == 0 else r + 1)
+    if r % 2:
+        keep = np.r_[0:6, 6:6 + r, 6 + r + 1:6 + r + 1 + r]
+        ops = g.Operators(K=ops.K[:r, :r], M=ops.M[:r, :r], b0=ops.b0[:r], b1=ops.b1[:r], N0=ops.N0, S=ops.S,
+                          H=ops.H[:, :r], G=ops.G[np.ix_(keep, keep)], nu=ops.nu, alpha=ops.alpha,
+                          alpha_lb=ops.alpha_lb)
+    omega = g.omega_grid(F)
+    for flags in (FLAG_OUT_R, FLAG_OUT_R | FLAG_MPT_PAIR):
+        res = run_gpu(torch, ops, omega, flags=flags)
+        assert (res["info"] == 0).all()
+        check_parity(ops, omega, res)
