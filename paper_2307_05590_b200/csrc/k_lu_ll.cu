@@ -95,7 +95,14 @@ struct Cfg {
   static constexpr int STRIP_TILES =
       TM ? NT + (HYB_G ? 0 : HYB_TILES) : (DIAG_L2 ? 1 + NT * (NT - 1) / 2 : NT * (NT + 1) / 2);
   static constexpr int MS = (R + 31) / 32;               // panel row slots per lane
-  static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16 * (TM ? 2 : 1);
+  // staging tile for the right-hand-side fragment conversions (rhs_frags through shared memory instead of shuffles):
+  // dev option, off -- fewer instructions but a longer back-substitution chain, r = 48: 2.518 vs 2.512 ms
+#ifdef PODP_LL_ZT
+  static constexpr int ZT_BYTES = TM ? 512 : 0;
+#else
+  static constexpr int ZT_BYTES = 0;
+#endif
+  static constexpr int W_BYTES = STRIP_TILES * 1024 + 9 * 16 + ((R * 4 + 15) / 16) * 16 * (TM ? 2 : 1) + ZT_BYTES;
   // KM (single-object launches, R <= 40, or with TM): K and M staged once per CTA in shared memory (row stride
   // R + 1 complex), so the column-tile gathers are shared-memory loads instead of L2 round trips (r = 40: 2.27 ->
   // 2.10 ms per 1e5 at the same 12 warps; without TM, at R >= 48 the copy would cost warps, measured slower)
@@ -212,9 +219,25 @@ __device__ __forceinline__ double frag_c2b(double c0, double c1, int s, int lane
 
 // Real-ified right-hand side tile Z = [Re z_0..2 | Im z_0..2 | 0 0] (C fragments) -> B fragments of Z (b1) and of
 // Z' = [-Im z | Re z | 0 0] (b2), so that a complex 8x8 A times z is  Re(A) Z + Im(A) Z'  (2 DMMA per k-step).
-__device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double (&b1)[2], double (&b2)[2]) {
+// zt != nullptr (tensor-memory variants): through a 512-byte row-major staging tile in shared memory (1 store + 4 loads
+// instead of 16 shuffles and their selects).
+__device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double (&b1)[2], double (&b2)[2],
+                                          double *zt = nullptr) {
   const int n = lane >> 2;
   const int j2 = n < 3 ? n + 3 : (n < 6 ? n - 3 : 6);
+  if (zt) {
+    __syncwarp();  // earlier loads from the tile are done
+    reinterpret_cast<double2 *>(zt)[lane] = make_double2(c0, c1);  // Z[lane / 4][2 (lane % 4) + {0, 1}]
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int k = 4 * s + (lane & 3);
+      b1[s] = zt[k * 8 + n];
+      const double w = zt[k * 8 + j2];
+      b2[s] = n < 3 ? -w : (n < 6 ? w : 0.0);
+    }
+    return;
+  }
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int row = 4 * (4 * s + (lane & 3));
@@ -234,9 +257,12 @@ __device__ __forceinline__ void rhs_frags(double c0, double c1, int lane, double
 // (Re(MY) = Ms Yr - Mi (Yr + Yi), Im(MY) = Ms Yr + Mr (Yi - Yr)): 6 DMMA per complex tile product instead of 8, for
 // one more accumulator set per column tile and 2 additions per M tile; ar/ai of tile B are final only as ar + ak,
 // ai + ak (formed here for Y_{B,c}, and by column_tile for the rows that go to the panel).
+// STG (tensor-memory variants): Y_{B,c} goes from C fragments to B fragments through one tile of the free
+// virtual strip (2 stores + 2 loads, XOR mask 2 (row & 3) | (row & 1): conflict-free both ways) instead of 16 shuffles
+// and 8 selects.
 template <int NT, int B, bool TM = false, bool M3 = false>
 __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], double (&ak)[NT][2], const double2 *S,
-                                     double2 *gY, int lane, uint32_t tm = 0) {
+                                     double2 *gY, int lane, uint32_t tm = 0, double2 *stg = nullptr) {
   if constexpr (M3) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -247,14 +273,35 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], d
   gY[2 * lane] = make_double2(ar[B][0], ai[B][0]);
   gY[2 * lane + 1] = make_double2(ar[B][1], ai[B][1]);
   double nyr[2], yi[2], nyi[2];  // M3: -Yr, Yr + Yi, Yr - Yi
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const double r = frag_c2b(ar[B][0], ar[B][1], s, lane), i = frag_c2b(ai[B][0], ai[B][1], s, lane);
-    nyr[s] = -r;
-    yi[s] = M3 ? r + i : i;
-    nyi[s] = M3 ? r - i : -i;
-  }
   const int r4 = lane >> 2, q = lane & 3;
+#ifndef PODP_LL_NO_STG
+  constexpr bool STG = TM;
+#else
+  constexpr bool STG = false;
+#endif
+  if constexpr (STG) {
+    const int fw = ((r4 & 3) << 1) | (r4 & 1);
+    __syncwarp();  // the previous block's loads from the staging tile are done
+    stg[r4 * 8 + ((2 * q) ^ fw)] = make_double2(ar[B][0], ai[B][0]);
+    stg[r4 * 8 + ((2 * q + 1) ^ fw)] = make_double2(ar[B][1], ai[B][1]);
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int k = 4 * s + q;  // B fragment: Y[k][n = r4]
+      const double2 y = stg[k * 8 + (r4 ^ (((k & 3) << 1) | (k & 1)))];
+      nyr[s] = -y.x;
+      yi[s] = M3 ? y.x + y.y : y.y;
+      nyi[s] = M3 ? y.x - y.y : -y.y;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double r = frag_c2b(ar[B][0], ar[B][1], s, lane), i = frag_c2b(ai[B][0], ai[B][1], s, lane);
+      nyr[s] = -r;
+      yi[s] = M3 ? r + i : i;
+      nyi[s] = M3 ? r - i : -i;
+    }
+  }
   constexpr int TB = Cfg<8 * NT, false, TM>::TM_TB;
   constexpr bool IN_TM = TM && B < TB;  // this strip in tensor memory (else shared memory)
   // TMEM loads in chunks of TMC tiles (one wait per chunk) to bound the registers they occupy
@@ -304,18 +351,20 @@ __device__ __forceinline__ void body(double (&ar)[NT][2], double (&ai)[NT][2], d
 
 template <int NT, bool TM = false, bool M3 = false, int B = 0>
 __device__ __forceinline__ void body_dispatch(int b, double (&ar)[NT][2], double (&ai)[NT][2], double (&ak)[NT][2],
-                                              const double2 *S, double2 *gY, int lane, uint32_t tm = 0) {
+                                              const double2 *S, double2 *gY, int lane, uint32_t tm = 0,
+                                              double2 *stg = nullptr) {
   if constexpr (B < NT - 1) {
-    if (b == B) body<NT, B, TM, M3>(ar, ai, ak, S, gY, lane, tm);
-    else body_dispatch<NT, TM, M3, B + 1>(b, ar, ai, ak, S, gY, lane, tm);
+    if (b == B) body<NT, B, TM, M3>(ar, ai, ak, S, gY, lane, tm, stg);
+    else body_dispatch<NT, TM, M3, B + 1>(b, ar, ai, ak, S, gY, lane, tm, stg);
   }
 }
 
 // Forward substitution z_t -= M_{t,B} z_B (real-ified right-hand side), t > B
 template <int NT, int B, bool TM = false>
-__device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, int lane, uint32_t tm = 0) {
+__device__ __forceinline__ void body_rhs(double (&z)[NT][2], const double2 *S, int lane, uint32_t tm = 0,
+                                         double *zt = nullptr) {
   double b1[2], b2[2];
-  rhs_frags(z[B][0], z[B][1], lane, b1, b2);
+  rhs_frags(z[B][0], z[B][1], lane, b1, b2, zt);
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     b1[s] = -b1[s];
@@ -647,8 +696,9 @@ __device__ __forceinline__ void column_tile(int c, double (&ar)[R / 8][2], doubl
   }
   if constexpr (!(PODP_LL_ABLATE & 2))
     for (int b = 0; b < c; ++b)
-      body_dispatch<NT, TM, M3>(b, ar, ai, ak, TM ? Sh : S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm);
+      body_dispatch<NT, TM, M3>(b, ar, ai, ak, TM ? Sh : S, gY + (c * (c - 1) / 2 + b) * 64, lane, tm, S);
   double2 *St = TM ? S : S + strip_off<C::DIAG_L2>(NT, c) * 64;
+  if constexpr (TM) __syncwarp();  // the last block's loads from the staging tile (strip tile 0) are done
 #pragma unroll
   for (int tt = 0; tt < NT; ++tt) {
     if (tt >= c) {
@@ -672,6 +722,7 @@ template <int R, bool TM = false>
 __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, double om, const double2 *S,
                                        double2 *gY, double2 *gD, const double2 *gDiag, const int *sPerm, double *Pw,
                                        int64_t t, int lane, uint32_t tm = 0, const double2 *sB = nullptr,
+                                       double *zt = nullptr,
                                        const double2 *Sh = nullptr) {
   using C = Cfg<R>;
   constexpr int NT = C::NT;
@@ -700,7 +751,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
   }
   if constexpr (!(PODP_LL_ABLATE & 8))
     [&]<int... Bs>(std::integer_sequence<int, Bs...>) {
-      (body_rhs<NT, Bs, TM>(z, TM ? Sh : S, lane, tm), ...);
+      (body_rhs<NT, Bs, TM>(z, TM ? Sh : S, lane, tm, zt), ...);
     }(std::make_integer_sequence<int, NT - 1>{});
   // ---- D_t = (L_tt U_tt)^{-1}: lane -> (tile t0 + lane/8, column lane%8); stored in C-fragment order -----------
   // DIAG_L2: the strips are no longer needed after the forward sweep, so the diagonal blocks are brought back from
@@ -760,7 +811,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
 #pragma unroll
   for (int tt = NT - 1; tt >= 0; --tt) {
     double b1[2], b2[2];
-    rhs_frags(z[tt][0], z[tt][1], lane, b1, b2);
+    rhs_frags(z[tt][0], z[tt][1], lane, b1, b2, zt);
     const double2 d0 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * DS, 0, lane) : afrag_cstore(gD + tt * 64, 0, lane);
     const double2 d1 = (C::DIAG_L2 || TM) ? afrag_cstore_s(sD + tt * DS, 1, lane) : afrag_cstore(gD + tt * 64, 1, lane);
     double x0 = 0.0, x1 = 0.0;
@@ -783,7 +834,7 @@ __device__ __forceinline__ void finish(const EvalArgs &a, const double *op, doub
       }
     }
     if (tt > 0 && !(PODP_LL_ABLATE & 8)) {
-      rhs_frags(x0, x1, lane, b1, b2);
+      rhs_frags(x0, x1, lane, b1, b2, zt);
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2) {
         b1[s2] = -b1[s2];
@@ -825,6 +876,8 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
   double2 *sRow = S + C::STRIP_TILES * 64;
   int *sPerm = reinterpret_cast<int *>(sRow + 9);
   int *sMap = sPerm + ((R + 3) / 4) * 4;  // TM: interchange source map (positions >= kb)
+  // TM: 512-byte staging tile of the right-hand-side fragment conversions (rhs_frags)
+  double *zt = C::ZT_BYTES ? reinterpret_cast<double *>(sMap + ((R + 3) / 4) * 4) : nullptr;
   const int64_t total = (int64_t)a.n_obj * a.F;
   const int64_t gw = (int64_t)blockIdx.x * G + wid, nw = (int64_t)gridDim.x * G;
   double2 *gY = a.gscr + (size_t)gw * C::GSCR_TILES * 64;  // Y_{t,c} at tile c(c-1)/2 + t; D_t at NT(NT-1)/2 + t
@@ -896,7 +949,7 @@ __global__ void __launch_bounds__(lull::Cfg<R, KM, TM>::G * 32, 1) lu_ll_kernel(
     }
     if (info == 0)
       lull::finish<R, TM>(a, op, om, S, gY, gD, gDiag, sPerm, Pw, t, lane, tm,
-                          C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr, Sh);
+                          C::KM_BYTES ? sKM + 2 * R * (R + 1) : nullptr, zt, Sh);
     if (valid) lull::fail_out(a, Pw, R, t, info, lane);
     __syncwarp();
   };
