@@ -158,7 +158,11 @@ podp_status podp_eval(const podp_ctx *ctx, const double *omega_d, int64_t F, dou
                       double *Delta_d, int32_t *info_d, double *P_d, int flags, void *cuda_stream);
 
 /* Host-buffer evaluation (the end-to-end entry point): copies omega host->device, runs podp_eval, copies the
- * outputs device->host and synchronises cuda_stream before returning.  Same shapes as podp_eval, all host. */
+ * outputs device->host and synchronises cuda_stream before returning.  Same shapes as podp_eval, all host.
+ * For one object and F >= 8192 the contraction runs as two launches over the halves of the frequency range and the
+ * first half's rows are copied back on a copy stream owned by the context while the second half is computed (same
+ * results bit for bit).  Host evaluations of one context are serialised among themselves (they share that stream);
+ * pinned host buffers make the copies asynchronous, pageable ones work too. */
 podp_status podp_eval_host(const podp_ctx *ctx, const double *omega_h, int64_t F, double *T1_h, double *I_h,
                            double *Delta_h, int32_t *info_h, int flags, void *cuda_stream);
 

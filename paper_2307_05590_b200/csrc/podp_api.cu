@@ -30,6 +30,10 @@ struct podp_ctx {
   // N1 literal per-direction form (podp_create_perdir): this context holds the concatenated cross-block operators
   // used by the contraction kernel; dir[i] holds direction i's system (M_i modes, padded to 8 ceil(M_i / 8)),
   // factored by its own solve launch
+  // podp_eval_host: copy stream and events of the overlapped device-to-host copy (created on first use)
+  std::mutex host_mu;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_half = nullptr, ev_copied = nullptr;
   podp_ctx *dir[3] = {nullptr, nullptr, nullptr};
   int m[3] = {0, 0, 0};
   int offp[3] = {0, 0, 0};  // direction block offsets in the padded (SL-aligned) concatenation
@@ -38,6 +42,19 @@ struct podp_ctx {
 namespace {
 
 thread_local std::string g_err;
+
+// podp_eval_host -> podp_eval: host destinations of the outputs.  When set (one object, default contraction kernel,
+// F >= 2 * HOST_SPLIT_MIN), the contraction runs as two launches over the halves of the frequency range and the first
+// half's rows are copied to the host on the context's copy stream while the second half is computed; F1 returns the
+// number of frequencies already copied.
+struct HostSplit {
+  double *T1_h, *I_h, *D_h;
+  cudaStream_t cs;
+  cudaEvent_t ev;
+  int64_t F1;
+};
+thread_local HostSplit *g_split = nullptr;
+constexpr int64_t HOST_SPLIT_MIN = 4096;
 
 // ---- benchmark instrumentation (podp_profile_*) ---------------------------------------------------------------
 struct ProfPair {
@@ -536,6 +553,11 @@ podp_status podp_destroy(podp_ctx *c) {
   // every stream's work on the context is complete after the device synchronisation; the operators go back to the
   // library pool (shared by every context on the device)
   cudaFreeAsync(c->d_ops, 0);
+  if (c->copy_stream) {
+    cudaStreamDestroy(c->copy_stream);
+    cudaEventDestroy(c->ev_half);
+    cudaEventDestroy(c->ev_copied);
+  }
   delete c;
   return PODP_OK;
 }
@@ -737,8 +759,34 @@ podp_status podp_eval(const podp_ctx *cc, const double *omega_d, int64_t F, doub
   }
   if (e == cudaSuccess) {
     ProfScope ps("mpt", s);
-    e = (flags & PODP_FLAG_MPT_GEMM) ? podp::launch_mpt_gemm(am, s, c->sms)
-                                     : podp::launch_mpt_tile(am, s, pencil_y && c->pencil_diag);
+    HostSplit *hs = g_split;
+    if (hs && c->n_obj == 1 && !(flags & PODP_FLAG_MPT_GEMM) && F >= 2 * HOST_SPLIT_MIN) {
+      // two launches over the halves (whole contraction tiles: no extra tail), first half's rows copied meanwhile
+      const int64_t F1 = (F / 2) / 64 * 64;
+      podp::EvalArgs a1 = am, a2 = am;
+      a1.F = F1;
+      a2.F = F - F1;
+      a2.omega += F1;
+      a2.Pws += (size_t)F1 * 3 * R;
+      a2.T1 += F1 * 6;
+      a2.I += F1 * 6;
+      a2.Delta += F1 * 6;
+      e = podp::launch_mpt_tile(a1, s, pencil_y && c->pencil_diag);
+      if (e == cudaSuccess) e = cudaEventRecord(hs->ev, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(hs->cs, hs->ev, 0);
+      const size_t nb = sizeof(double) * (size_t)F1 * 6;
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hs->T1_h, am.T1, nb, cudaMemcpyDeviceToHost, hs->cs);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hs->I_h, am.I, nb, cudaMemcpyDeviceToHost, hs->cs);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(hs->D_h, am.Delta, nb, cudaMemcpyDeviceToHost, hs->cs);
+      if (e == cudaSuccess) {
+        ++nl;
+        hs->F1 = F1;
+        e = podp::launch_mpt_tile(a2, s, pencil_y && c->pencil_diag);
+      }
+    } else {
+      e = (flags & PODP_FLAG_MPT_GEMM) ? podp::launch_mpt_gemm(am, s, c->sms)
+                                       : podp::launch_mpt_tile(am, s, pencil_y && c->pencil_diag);
+    }
     if (e == cudaSuccess) ++nl;
   }
   cudaFreeAsync(a.Pws, s);
@@ -771,14 +819,43 @@ podp_status podp_eval_host(const podp_ctx *c, const double *omega_h, int64_t F, 
   int32_t *info = (int32_t *)(buf + b_om + 3 * b_out);
   e = cudaMemcpyAsync(om, omega_h, sizeof(double) * F, cudaMemcpyHostToDevice, s);
   podp_status st = PODP_OK;
+  bool split_used = false;
+  podp_ctx *cw = const_cast<podp_ctx *>(c);
+  // host evaluations of one context share its copy stream and events: they are serialised (they would share the GPU
+  // anyway); device-pointer evaluations (podp_eval) stay fully concurrent
+  std::lock_guard<std::mutex> host_lk(cw->host_mu);
   if (e == cudaSuccess) {
+    // the first half of the outputs is copied back on the context's copy stream while the contraction kernel works
+    // on the second half (podp_eval, HostSplit)
+    HostSplit hs{T1_h, I_h, Delta_h, nullptr, nullptr, 0};
+    {
+      if (!cw->copy_stream) {
+        if (cudaStreamCreateWithFlags(&cw->copy_stream, cudaStreamNonBlocking) != cudaSuccess) cw->copy_stream = nullptr;
+        if (cw->copy_stream && (cudaEventCreateWithFlags(&cw->ev_half, cudaEventDisableTiming) != cudaSuccess ||
+                                cudaEventCreateWithFlags(&cw->ev_copied, cudaEventDisableTiming) != cudaSuccess)) {
+          cudaStreamDestroy(cw->copy_stream);
+          cw->copy_stream = nullptr;
+        }
+      }
+      hs.cs = cw->copy_stream;
+      hs.ev = cw->ev_half;
+    }
+    g_split = hs.cs ? &hs : nullptr;
     st = podp_eval(c, om, F, T1, I, D, info_h ? info : nullptr, nullptr, flags, s);
+    g_split = nullptr;
+    const int64_t F1 = hs.F1;  // frequencies already on their way to the host (one object)
+    split_used = F1 > 0;
     if (st == PODP_OK) {
-      e = cudaMemcpyAsync(T1_h, T1, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(I_h, I, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(Delta_h, D, sizeof(double) * nout, cudaMemcpyDeviceToHost, s);
+      const size_t off = (size_t)F1 * 6, nb = sizeof(double) * (nout - off);
+      e = cudaMemcpyAsync(T1_h + off, T1 + off, nb, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(I_h + off, I + off, nb, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(Delta_h + off, D + off, nb, cudaMemcpyDeviceToHost, s);
       if (e == cudaSuccess && info_h)
         e = cudaMemcpyAsync(info_h, info, sizeof(int32_t) * c->n_obj * F, cudaMemcpyDeviceToHost, s);
+    }
+    if (split_used) {  // the staging buffer is released (stream-ordered on s) only after the copy stream is done
+      cudaEventRecord(cw->ev_copied, cw->copy_stream);
+      cudaStreamWaitEvent(s, cw->ev_copied, 0);
     }
   }
   cudaFreeAsync(buf, s);

@@ -328,6 +328,30 @@ def test_eval_host_batch_nan(torch_cuda):
     ev.close()
 
 
+@pytest.mark.parametrize("r,F", [(8, 8192), (24, 20_001), (48, 9_999)])
+def test_eval_host_overlapped_copy(torch_cuda, r, F):
+    """One object and F >= 8192: podp_eval_host runs the contraction as two launches and copies the first half of the
+    outputs back while the second half is computed.  Results (with failed frequencies in both halves and at the
+    split) must equal the device entry bit for bit, and a second call on the same context must too."""
+    torch = torch_cuda
+    from paper_2307_05590_b200 import Evaluator, FLAG_OUT_R
+    ops = g.make_operators(r)
+    omega = g.omega_grid(F)
+    F1 = (F // 2) // 64 * 64
+    for k in (5, F1 - 1, F1, F - 2):
+        omega[k] = np.nan
+    ev = Evaluator(ops)
+    d = ev.eval(torch.tensor(omega, device="cuda"), flags=FLAG_OUT_R)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        h = ev.eval_host(omega, flags=FLAG_OUT_R)
+        for k in ("T1", "I", "Delta"):
+            assert np.array_equal(h[k], d[k].cpu().numpy(), equal_nan=True), k
+        assert np.array_equal(h["info"], d["info"].cpu().numpy())
+    assert (h["info"][0, [5, F1 - 1, F1, F - 2]] == -1).all() and np.isnan(h["T1"][0, F1]).all()
+    ev.close()
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_full_size_configs_sampled(torch_cuda, cfg):
