@@ -24,6 +24,11 @@
 //   Shared memory per warp holds only the M tiles (NT(NT-1)/2) plus one tile for the current panel's diagonal block
 //   (see strip_off): the diagonal blocks go to the L2 scratch with the Y tiles, which buys warps per SM (r = 48:
 //   12 instead of 10, r = 96: 3 instead of 2; measured 3.47 -> 3.29 ms and 48.4 -> 33.1 ms per 1e5 frequencies).
+//   Round-2 additions (each measured): M tiles in TENSOR MEMORY with K and M staged in shared
+//   memory (Cfg::TM), strips beyond tensor memory in the L2 scratch (HYB_G), a CTA rendezvous every 16th frequency at
+//   R = 48 so that the warps share the instruction cache (LOCKSTEP), Gauss's three-product complex multiplication in
+//   the updates (GAUSS3), conflict-free strip swizzle and padded staging of the diagonal blocks, Y tiles converted
+//   from C to B fragments through a free strip tile (body, stg).
 #include <utility>
 
 #include "podp_common.cuh"
