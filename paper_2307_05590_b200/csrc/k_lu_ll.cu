@@ -134,11 +134,12 @@ struct Cfg {
   // 0.5-8 %; R >= 56: 0-1.5 %), so only the R = 48 tensor-memory variant takes it.
   // GAUSS3: three-product complex tile multiplication in the left-looking updates (see body): 330 instead of 440
   // DMMA per frequency at r = 48.  Measured per 1e5: r = 40 2.07 -> 1.95 ms, r = 48 2.76 -> 2.68, r = 64 5.45 -> 5.38,
-  // r = 32 1.18 -> 1.17; not faster at r <= 24 (few updates) and slower at r = 96 (20.1 vs 19.7: registers)
+  // r = 32 1.18 -> 1.17, r = 72 8.08 -> 8.02, r = 80 10.31 -> 10.09; not faster at r <= 24 (few updates) and slower at
+  // r = 88 (16.39 vs 16.16) and r = 96 (20.1 vs 19.7): registers
 #ifdef PODP_LL_GAUSS3
   static constexpr bool GAUSS3 = PODP_LL_GAUSS3 != 0;
 #else
-  static constexpr bool GAUSS3 = R >= 32 && R <= 64;
+  static constexpr bool GAUSS3 = R >= 32 && R <= 80;
 #endif
 #ifdef PODP_LL_SYNC
   static constexpr bool LOCKSTEP = PODP_LL_SYNC != 0;

@@ -1,6 +1,6 @@
 // Device helpers shared by the libpodp kernels (complex FP64 arithmetic on double2 = (re, im)).
 // Every complex multiply-add here is 4 DFMA.  (Gauss's three-product form is used only in the DMMA trailing updates of
-// the left-looking LU for 32 <= R <= 64, k_lu_ll.cu body<M3>; DESIGN reading B14 has the measured parity margins.)
+// the left-looking LU for 32 <= R <= 80, k_lu_ll.cu body<M3>; DESIGN reading B14 has the measured parity margins.)
 #pragma once
 #include <cuda_runtime.h>
 #include "podp_internal.h"
